@@ -1,0 +1,104 @@
+// C-ABI plumbing: thread-local last error, device queries, and small utility kernels
+// (finite check for ParamTable, toy_env.py:71-72; ascent_step add, objective.py:286-293).
+#include "common.cuh"
+#include "capi_internal.h"
+
+namespace rlk {
+
+static thread_local char g_last_error[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return RLK_OK;
+  set_error("%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+  return RLK_ERR_CUDA;
+}
+
+int launch_status(const char* where) { return cuda_status(cudaGetLastError(), where); }
+
+int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+template <int DT>
+__global__ void k_nonfinite(const void* __restrict__ x, uint64_t n, unsigned long long* count) {
+  uint64_t local = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v = load_f64<DT>(x, i);
+    local += !isfinite(v);
+  }
+  unsigned int c = (unsigned int)local;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
+template <int DT>
+__global__ void k_scaled_add(const void* __restrict__ a, const void* __restrict__ b, double alpha,
+                             void* __restrict__ out, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    // objective.py:293: params.logits + lr * gradient (two f64 roundings, no FMA contraction)
+    double v = __dadd_rn(load_f64<DT>(a, i), __dmul_rn(alpha, load_f64<DT>(b, i)));
+    store_from_f64<DT>(out, i, v);
+  }
+}
+
+}  // namespace rlk
+
+using namespace rlk;
+
+extern "C" {
+
+const char* rlk_last_error(void) { return g_last_error; }
+
+int rlk_abi_version(void) { return 1; }
+
+int rlk_device_sm_count(int device) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return n;
+}
+
+int rlk_nonfinite_count(const void* x, int dtype, uint64_t n, unsigned long long* count, void* stream) {
+  RLK_REQUIRE(count != nullptr, "rlk_nonfinite_count: count is NULL");
+  if (n == 0) return RLK_OK;
+  RLK_REQUIRE(x != nullptr, "rlk_nonfinite_count: x is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t blocks = (n + 255) / 256;
+  int grid = (int)(blocks < (uint64_t)sm_count() * 8 ? blocks : (uint64_t)sm_count() * 8);
+  switch (dtype) {
+    case RLK_BF16: k_nonfinite<RLK_BF16><<<grid, 256, 0, s>>>(x, n, count); break;
+    case RLK_F32: k_nonfinite<RLK_F32><<<grid, 256, 0, s>>>(x, n, count); break;
+    case RLK_F64: k_nonfinite<RLK_F64><<<grid, 256, 0, s>>>(x, n, count); break;
+    default: set_error("rlk_nonfinite_count: bad dtype %d", dtype); return RLK_ERR_INVALID;
+  }
+  return launch_status("rlk_nonfinite_count");
+}
+
+int rlk_scaled_add(const void* a, const void* b, double alpha, void* out, int dtype, uint64_t n,
+                   void* stream) {
+  if (n == 0) return RLK_OK;
+  RLK_REQUIRE(a && b && out, "rlk_scaled_add: NULL pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t blocks = (n + 255) / 256;
+  int grid = (int)(blocks < (uint64_t)sm_count() * 8 ? blocks : (uint64_t)sm_count() * 8);
+  switch (dtype) {
+    case RLK_BF16: k_scaled_add<RLK_BF16><<<grid, 256, 0, s>>>(a, b, alpha, out, n); break;
+    case RLK_F32: k_scaled_add<RLK_F32><<<grid, 256, 0, s>>>(a, b, alpha, out, n); break;
+    case RLK_F64: k_scaled_add<RLK_F64><<<grid, 256, 0, s>>>(a, b, alpha, out, n); break;
+    default: set_error("rlk_scaled_add: bad dtype %d", dtype); return RLK_ERR_INVALID;
+  }
+  return launch_status("rlk_scaled_add");
+}
+
+}  // extern "C"

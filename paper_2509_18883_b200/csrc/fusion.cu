@@ -1,0 +1,789 @@
+// Task-vector fusion kernels for sm_100a (K1 norm partials, finalize, K2 dropout bitmap, K3 merge).
+//
+// Reference algorithm (pkg/src/rolloutlab/fusion.py):
+//   task_vector           79-83    delta = expert - base (f64, exact for bf16/f32 inputs)
+//   TaskVector.norm       37-44    ||delta||_2
+//   normalize_magnitudes  86-102   target = mean of non-zero norms | fixed | None; delta * (target / norm)
+//   dropout_prune        105-115   keep iff uniform >= p (SplitMix64 stream rng.split(i)), survivors / (1 - p)
+//   erase_minority       118-142   majority = sign(sum_i k_i) or sign(sum_i sign(k_i) k_i^2); zero opposers
+//   fuse                 154-188   fused = base; fused = fused + w_i * k_i (sequential), FusionStats
+//
+// Both passes are persistent, warp-specialised TMA pipelines: one producer warp issues 1-D bulk
+// copies (cp.async.bulk -> SASS UBLKCP) of every stream's stage tile into a shared-memory ring,
+// completion tracked by mbarrier transaction counts; eight consumer warps read the stage with 128-bit
+// LDS, compute, and release the slot.  Grid = one CTA per SM, items strided over CTAs.
+#include "common.cuh"
+#include "capi_internal.h"
+#include "pipeline.cuh"
+
+namespace rlk {
+
+constexpr uint32_t kItem = RLK_FUSION_ITEM;
+constexpr uint32_t kSmemBudget = 210 * 1024;
+
+template <int N> struct StreamBytes { static constexpr uint32_t v = N <= 4 ? 8192u : 4096u; };
+
+struct ItemGeom {
+  const rlk_fusion_segment* seg;
+  uint64_t start;  // element offset of the item within its piece
+  uint32_t len;
+  uint32_t gitem;
+  uint32_t tensor;
+};
+
+__device__ __forceinline__ ItemGeom item_geom(const rlk_fusion_plan& plan, uint32_t item) {
+  uint32_t lo = 0, hi = plan.n_segs;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(plan.seg_item_prefix + mid) <= item) lo = mid; else hi = mid;
+  }
+  ItemGeom g;
+  g.seg = plan.segs + lo;
+  uint32_t k = item - __ldg(plan.seg_item_prefix + lo);
+  g.start = (uint64_t)k * kItem;
+  uint64_t rem = g.seg->numel - g.start;
+  g.len = rem < kItem ? (uint32_t)rem : kItem;
+  g.gitem = g.seg->item0 + k;
+  g.tensor = g.seg->tensor;
+  return g;
+}
+
+// Producer: one elected lane streams every (item, stage) of this CTA through the ring.
+// Stage layout: [stream 0 | stream 1 | ... | stream NS-1 | bitmap expert 0 | ... | bitmap expert N-1].
+template <int ESZ, int N>
+__device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_base, const uint32_t* bitmap,
+                        uint64_t words_per_row) {
+  constexpr uint32_t SB = StreamBytes<N>::v;
+  constexpr uint32_t ELEMS = SB / ESZ;
+  constexpr uint32_t BMB = ELEMS / 8;  // bitmap bytes per expert per full stage
+  const int ns = with_base ? N + 1 : N;
+  const uint64_t pol = policy_evict_first();
+  uint32_t q = 0;
+  for (uint32_t item = blockIdx.x; item < plan.n_items; item += gridDim.x) {
+    const ItemGeom g = item_geom(plan, item);
+    const char* src[N + 1];
+    if (!with_base) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) src[i] = (const char*)g.seg->expert[i];
+    } else {
+      src[0] = (const char*)g.seg->base;
+#pragma unroll
+      for (int i = 0; i < N; ++i) src[i + 1] = (const char*)g.seg->expert[i];
+    }
+    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    for (uint32_t off = 0; off < g.len; off += ELEMS) {
+      const uint32_t n = min(ELEMS, g.len - off);
+      const uint32_t main_bytes = (n * ESZ) & ~15u;
+      const uint32_t bm_bytes = bitmap ? (((n + 7) / 8 + 15) & ~15u) : 0u;
+      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      mbar_wait(&r.empty[s], ph ^ 1u);
+      const uint32_t tx = main_bytes * ns + bm_bytes * N;
+      uint8_t* dst = r.buf + s * r.stage_bytes;
+      if (tx) {
+        mbar_arrive_expect_tx(&r.full[s], tx);
+        if (main_bytes) {
+          const uint64_t byte_off = (g.start + off) * ESZ;
+          for (int k = 0; k < ns; ++k) bulk_g2s(dst + k * SB, src[k] + byte_off, main_bytes, &r.full[s], pol);
+        }
+        if (bm_bytes) {
+          const uint64_t jb = jtensor0 + off;  // multiple of ELEMS -> byte offset multiple of 16
+          for (int i = 0; i < N; ++i)
+            bulk_g2s(dst + (N + 1) * SB + i * BMB, (const char*)(bitmap + i * words_per_row) + jb / 8, bm_bytes,
+                     &r.full[s], pol);
+        }
+      } else {
+        mbar_arrive(&r.full[s]);
+      }
+      ++q;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ vector unpack helpers
+template <int DT> struct VecIO;
+template <> struct VecIO<RLK_BF16> {
+  static constexpr int n = 8;
+  __device__ static void f32(const uint4& w, float* o) {
+    o[0] = bf16_lo(w.x); o[1] = bf16_hi(w.x); o[2] = bf16_lo(w.y); o[3] = bf16_hi(w.y);
+    o[4] = bf16_lo(w.z); o[5] = bf16_hi(w.z); o[6] = bf16_lo(w.w); o[7] = bf16_hi(w.w);
+  }
+  __device__ static void f64(const uint4& w, double* o) {
+    float t[8];
+    f32(w, t);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = (double)t[e];
+  }
+};
+template <> struct VecIO<RLK_F32> {
+  static constexpr int n = 4;
+  __device__ static void f64(const uint4& w, double* o) {
+    o[0] = (double)__uint_as_float(w.x); o[1] = (double)__uint_as_float(w.y);
+    o[2] = (double)__uint_as_float(w.z); o[3] = (double)__uint_as_float(w.w);
+  }
+};
+template <> struct VecIO<RLK_F64> {
+  static constexpr int n = 2;
+  __device__ static void f64(const uint4& w, double* o) {
+    o[0] = __hiloint2double((int)w.y, (int)w.x);
+    o[1] = __hiloint2double((int)w.w, (int)w.z);
+  }
+};
+
+// Store VEC outputs (given as f64) at element index idx of out (vectorised when aligned).
+template <int DTO, int VEC>
+__device__ __forceinline__ void store_vec_f64(void* out, uint64_t idx, const double* y) {
+  if constexpr (DTO == RLK_BF16) {
+    uint32_t h[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) h[e] = f64_to_bf16_rne(y[e]);
+    if constexpr (VEC == 8) {
+      uint4 w = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+      stg128_stream((uint16_t*)out + idx, w);
+    } else if constexpr (VEC == 4) {
+      *reinterpret_cast<uint2*>((uint16_t*)out + idx) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+    } else {
+      *reinterpret_cast<uint32_t*>((uint16_t*)out + idx) = h[0] | (h[1] << 16);
+    }
+  } else if constexpr (DTO == RLK_F32) {
+    float f[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) f[e] = f64_to_f32_rn(y[e]);
+#pragma unroll
+    for (int e = 0; e < VEC; e += 4) {
+      if constexpr (VEC >= 4) {
+        stg128_stream((float*)out + idx + e, make_uint4(__float_as_uint(f[e]), __float_as_uint(f[e + 1]),
+                                                         __float_as_uint(f[e + 2]), __float_as_uint(f[e + 3])));
+      }
+    }
+    if constexpr (VEC == 2) *reinterpret_cast<float2*>((float*)out + idx) = make_float2(f[0], f[1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; e += 2) {
+      stg128_stream((double*)out + idx + e,
+                    make_uint4(__double2loint(y[e]), __double2hiint(y[e]), __double2loint(y[e + 1]),
+                               __double2hiint(y[e + 1])));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K1: norm partials
+template <int DT, int N>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_sumsq(rlk_fusion_plan plan, int delta_mode, double* __restrict__ partials, uint32_t stage_bytes,
+            uint32_t nstages) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int ESZ = Elem<DT>::size;
+  constexpr int VEC = 16 / ESZ;
+  constexpr uint32_t SB = StreamBytes<N>::v;
+  constexpr uint32_t ELEMS = SB / ESZ;
+  const Ring r = ring_setup(smem, stage_bytes, nstages);
+  const bool delta = delta_mode != 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == kCWarps) {
+    if (lane == 0) produce<ESZ, N>(plan, r, !delta, nullptr, 0);
+    return;
+  }
+  __shared__ double red[kCWarps][N];
+  const int tid = threadIdx.x;
+  uint32_t q = 0;
+  for (uint32_t item = blockIdx.x; item < plan.n_items; item += gridDim.x) {
+    const ItemGeom g = item_geom(plan, item);
+    double acc[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = 0.0;
+    for (uint32_t off = 0; off < g.len; off += ELEMS) {
+      const uint32_t n = min(ELEMS, g.len - off);
+      const uint32_t main_elems = ((n * ESZ) & ~15u) / ESZ;
+      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      mbar_wait(&r.full[s], ph);
+      const uint8_t* sb = r.buf + s * r.stage_bytes;
+      const uint32_t nvec = main_elems / VEC;
+      for (uint32_t v = tid; v < nvec; v += kCThreads) {
+        double b[VEC];
+        if (!delta) VecIO<DT>::f64(lds128(sb + v * 16), b);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double x[VEC];
+          VecIO<DT>::f64(lds128(sb + (i + (delta ? 0 : 1)) * SB + v * 16), x);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double d = delta ? x[e] : x[e] - b[e];
+            acc[i] = fma(d, d, acc[i]);
+          }
+        }
+      }
+      for (uint32_t e = main_elems + tid; e < n; e += kCThreads) {
+        const uint64_t idx = g.start + off + e;
+        const double b = delta ? 0.0 : load_f64<DT>(g.seg->base, idx);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double x = load_f64<DT>(g.seg->expert[i], idx);
+          const double d = delta ? x : x - b;
+          acc[i] = fma(d, d, acc[i]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r.empty[s]);
+      ++q;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double w = warp_sum_f64(acc[i]);
+      if (lane == 0) red[warp][i] = w;
+    }
+    cbar_sync();
+    if (tid < N) {
+      double t = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kCWarps; ++w) t += red[w][tid];
+      partials[(uint64_t)g.gitem * N + tid] = t;
+    }
+    cbar_sync();
+  }
+}
+
+// ------------------------------------------------------------------ finalize: norms -> scales
+// One warp per tensor; lane l sums items l, l+32, ... then a fixed xor-tree: the result depends only
+// on the global item partition, never on which rank produced which partial.
+__global__ void k_finalize(const double* __restrict__ partials, const uint32_t* __restrict__ tensor_items,
+                           uint32_t n_tensors, int n, int target_mode, double target_value,
+                           double* __restrict__ sumsq, double* __restrict__ scale, int32_t* __restrict__ status) {
+  const uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= n_tensors) return;
+  const uint32_t i0 = tensor_items[t], i1 = tensor_items[t + 1];
+  double norms[RLK_MAX_EXPERTS];
+  bool finite = true;
+  for (int i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (uint32_t k = i0 + lane; k < i1; k += 32) acc += partials[(uint64_t)k * n + i];
+    acc = warp_sum_f64(acc);
+    finite = finite && isfinite(acc);
+    norms[i] = sqrt(acc);  // IEEE correctly rounded (np.linalg.norm = sqrt(dot))
+    if (lane == 0) sumsq[(uint64_t)t * n + i] = acc;
+  }
+  if (lane != 0) return;
+  int32_t st = finite ? 0 : 2;
+  double target = 1.0;
+  if (target_mode == 1) {  // fusion.py:95-99: mean of the non-zero norms (Python sum order)
+    double sum = 0.0;
+    int cnt = 0;
+    for (int i = 0; i < n; ++i)
+      if (norms[i] > 0.0) { sum = sum + norms[i]; ++cnt; }
+    if (cnt == 0 && st == 0) st = 1;
+    target = cnt ? sum / (double)cnt : 0.0;
+  } else if (target_mode == 2) {
+    target = target_value;
+  }
+  for (int i = 0; i < n; ++i) {
+    // fusion.py:102: zero vectors pass through; otherwise delta * (target / norm)
+    const double sc = (target_mode == 0 || norms[i] == 0.0) ? 1.0 : target / norms[i];
+    scale[(uint64_t)t * n + i] = sc;
+  }
+  status[t] = st;
+}
+
+// ------------------------------------------------------------------ K2: dropout keep bitmap
+__global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, uint64_t thresh, uint64_t n_bits,
+                              uint32_t* __restrict__ bitmap, uint64_t words_per_row) {
+  const uint64_t words = (n_bits + 31) / 32;
+  const uint64_t total = words * (uint64_t)n;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t gw = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; gw < total; gw += stride) {
+    const int i = (int)(gw / words);
+    const uint64_t w = gw - (uint64_t)i * words;
+    const uint64_t seed = i < 4 ? (&seeds_lo.x)[i] : (&seeds_hi.x)[i - 4];
+    uint32_t bits = 0;
+    const uint64_t j0 = w * 32;
+#pragma unroll 8
+    for (int b = 0; b < 32; ++b) bits |= (uint32_t)keep_draw(seed, j0 + b, thresh) << b;
+    bitmap[(uint64_t)i * words_per_row + w] = bits;
+  }
+}
+
+// ------------------------------------------------------------------ K3: merge
+struct MergeArgs {
+  rlk_fusion_plan plan;
+  const double* scale;  // [n_tensors * N]
+  double w[RLK_MAX_EXPERTS];
+  uint64_t seed[RLK_MAX_EXPERTS];
+  uint64_t thresh;
+  double keep_prob, inv_keep;
+  uint64_t words_per_row;
+  unsigned long long* counters;
+  int dropout_mode, erase_mode, delta_mode, with_base, fast;
+  uint32_t stage_bytes, nstages;
+  const uint32_t* bitmap;
+};
+
+struct ElemConsts {
+  double scale[RLK_MAX_EXPERTS];
+};
+
+// RN(a / b) from r = RN(1/b): q = RN(a r); e = a - q b (exact by FMA); RN(q + e r) (Markstein).
+__device__ __forceinline__ double div_rn(double a, double b, double r) {
+  const double q = __dmul_rn(a, r);
+  const double e = fma(-q, b, a);
+  return fma(e, r, q);
+}
+
+// Reference-order f64 evaluation of one element (exact semantics of fusion.py:102, 114, 130-141, 184-186).
+// keep: bit i = dropout keep decision of expert i.  Returns fused value; nz/er: bit i set when
+// expert i's entry is non-zero after dropout / was erased.
+template <int N>
+__device__ __forceinline__ double merge_elem_f64(double B, const double* X, uint32_t keep, const MergeArgs& a,
+                                                 const ElemConsts& c, uint32_t& nz, uint32_t& er) {
+  double K[N];
+  nz = 0;
+  er = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double D = a.delta_mode ? X[i] : __dsub_rn(X[i], B);
+    double k = __dmul_rn(D, c.scale[i]);
+    if (a.dropout_mode) k = ((keep >> i) & 1u) ? div_rn(k, a.keep_prob, a.inv_keep) : 0.0;
+    K[i] = k;
+    nz |= (uint32_t)(k != 0.0) << i;
+  }
+  if (N >= 2 && a.erase_mode) {
+    double V;
+    if (a.erase_mode == 1) {
+      V = K[0];
+#pragma unroll
+      for (int i = 1; i < N; ++i) V = __dadd_rn(V, K[i]);
+    } else {
+      auto sq = [](double k) {
+        const double s = k > 0.0 ? 1.0 : (k < 0.0 ? -1.0 : (k == 0.0 ? 0.0 : k));
+        return __dmul_rn(s, __dmul_rn(k, k));
+      };
+      V = sq(K[0]);
+#pragma unroll
+      for (int i = 1; i < N; ++i) V = __dadd_rn(V, sq(K[i]));
+    }
+    const int maj = V > 0.0 ? 1 : (V < 0.0 ? -1 : 0);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const bool opp = (maj > 0 && K[i] < 0.0) || (maj < 0 && K[i] > 0.0);
+      if (opp) {
+        K[i] = 0.0;
+        er |= 1u << i;
+      }
+    }
+  }
+  double Y = B;
+#pragma unroll
+  for (int i = 0; i < N; ++i) Y = __dadd_rn(Y, __dmul_rn(a.w[i], K[i]));
+  return Y;
+}
+
+template <int N, int VEC>
+__device__ __forceinline__ uint32_t keep_bits_for(const MergeArgs& a, const uint8_t* bm_stage, uint32_t bm_stride,
+                                                  uint32_t local_elem, uint64_t jglobal, int e) {
+  // returns N-bit keep mask for element local_elem + e
+  uint32_t m = 0;
+  if (a.dropout_mode == 0) return (1u << N) - 1u;
+  if (a.dropout_mode == 2) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint32_t word = reinterpret_cast<const uint32_t*>(bm_stage + i * bm_stride)[(local_elem + e) >> 5];
+      m |= ((word >> ((local_elem + e) & 31)) & 1u) << i;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) m |= (uint32_t)keep_draw(a.seed[i], jglobal + e, a.thresh) << i;
+  }
+  return m;
+}
+
+template <int DTI, int DTO, int N>
+__global__ void __launch_bounds__(kThreads, 1) k_merge(MergeArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int ESZ = Elem<DTI>::size;
+  constexpr int VEC = 16 / ESZ;
+  constexpr uint32_t SB = StreamBytes<N>::v;
+  constexpr uint32_t ELEMS = SB / ESZ;
+  constexpr uint32_t BMB = ELEMS / 8;
+  const Ring r = ring_setup(smem, a.stage_bytes, a.nstages);
+  const bool delta = a.delta_mode != 0;
+  const bool wb = a.with_base != 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == kCWarps) {
+    if (lane == 0) produce<ESZ, N>(a.plan, r, wb, a.dropout_mode == 2 ? a.bitmap : nullptr, a.words_per_row);
+    return;
+  }
+  const int tid = threadIdx.x;
+  uint32_t q = 0;
+  for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
+    const ItemGeom g = item_geom(a.plan, item);
+    ElemConsts c;
+    float sr32[N], w32[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      c.scale[i] = __ldg(a.scale + (uint64_t)g.tensor * N + i);
+      sr32[i] = (float)(a.dropout_mode ? c.scale[i] / a.keep_prob : c.scale[i]);
+      w32[i] = (float)a.w[i];
+    }
+    uint32_t cnt_nz[N], cnt_er[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) cnt_nz[i] = cnt_er[i] = 0;
+    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    for (uint32_t off = 0; off < g.len; off += ELEMS) {
+      const uint32_t n = min(ELEMS, g.len - off);
+      const uint32_t main_elems = ((n * ESZ) & ~15u) / ESZ;
+      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      mbar_wait(&r.full[s], ph);
+      const uint8_t* sb = r.buf + s * r.stage_bytes;
+      const uint8_t* bm = sb + (N + 1) * SB;
+      const uint32_t nvec = main_elems / VEC;
+      const uint64_t out_base = g.start + off;
+      for (uint32_t v = tid; v < nvec; v += kCThreads) {
+        const uint32_t le = v * VEC;
+        if constexpr (DTI == RLK_BF16 && DTO == RLK_BF16) {
+          if (a.fast) {
+            // ---- f32 fast path with certified guards; falls back to merge_elem_f64 per element.
+            float b[8], x[N][8];
+            if (wb) VecIO<RLK_BF16>::f32(lds128(sb + v * 16), b);
+            else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) b[e] = 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < N; ++i) VecIO<RLK_BF16>::f32(lds128(sb + (i + (wb ? 1 : 0)) * SB + v * 16), x[i]);
+            uint32_t kb[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              if (a.dropout_mode == 2) kb[i] = bm[i * BMB + (le >> 3)];
+              else if (a.dropout_mode == 1) {
+                kb[i] = 0;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) kb[i] |= (uint32_t)keep_draw(a.seed[i], jtensor0 + off + le + e, a.thresh) << e;
+              } else kb[i] = 0xffu;
+            }
+            float y[8];
+            uint32_t slowmask = 0, slowbits[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              float d[N], k[N];
+              uint32_t nzm = 0, erm = 0;
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                d[i] = delta ? x[i][e] : x[i][e] - b[e];
+                const bool keep = (kb[i] >> e) & 1u;
+                nzm |= (uint32_t)(keep && d[i] != 0.f) << i;
+                k[i] = keep ? d[i] * sr32[i] : 0.f;
+              }
+              bool slow = false;
+              if (N >= 2 && a.erase_mode) {
+                float vv = 0.f, A = 0.f;
+                if (a.erase_mode == 1) {
+                  vv = k[0];
+                  A = fabsf(k[0]);
+#pragma unroll
+                  for (int i = 1; i < N; ++i) { vv += k[i]; A += fabsf(k[i]); }
+                  slow = !(fabsf(vv) > 0x1p-20f * A);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < N; ++i) {
+                    const float q2 = k[i] * k[i];
+                    vv += copysignf(q2, k[i]);
+                    A += q2;
+                  }
+                  slow = !(fabsf(vv) > 0x1p-19f * A);
+                }
+                const uint32_t vs = __float_as_uint(vv) & 0x80000000u;
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                  const bool opp = ((nzm >> i) & 1u) && ((__float_as_uint(d[i]) & 0x80000000u) != vs);
+                  if (opp) k[i] = 0.f;
+                  erm |= (uint32_t)opp << i;
+                }
+              }
+              float yy = b[e], S = fabsf(b[e]);
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                yy = fmaf(w32[i], k[i], yy);
+                S = fmaf(w32[i], fabsf(k[i]), S);
+              }
+              const float mid = __uint_as_float((__float_as_uint(yy) & 0xffff0000u) | 0x8000u);
+              slow = slow || !(fabsf(yy - mid) > 0x1p-19f * S);
+              y[e] = yy;
+              if (slow) {
+                // certified guard tripped: exact reference-order evaluation of this element
+                double X[N];
+                uint32_t keep = 0;
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                  X[i] = (double)x[i][e];
+                  keep |= ((kb[i] >> e) & 1u) << i;
+                }
+                const double Y = merge_elem_f64<N>((double)b[e], X, keep, a, c, nzm, erm);
+                slowbits[e] = f64_to_bf16_rne(Y);
+                slowmask |= 1u << e;
+              }
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                cnt_nz[i] += (nzm >> i) & 1u;
+                cnt_er[i] += (erm >> i) & 1u;
+              }
+            }
+            uint32_t outw[4];
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              __nv_bfloat162 p2 = __floats2bfloat162_rn(y[2 * e2], y[2 * e2 + 1]);
+              uint32_t w = *reinterpret_cast<uint32_t*>(&p2);
+              if (slowmask & (1u << (2 * e2))) w = (w & 0xffff0000u) | slowbits[2 * e2];
+              if (slowmask & (2u << (2 * e2))) w = (w & 0x0000ffffu) | (slowbits[2 * e2 + 1] << 16);
+              outw[e2] = w;
+            }
+            stg128_stream((uint16_t*)g.seg->out + out_base + le, make_uint4(outw[0], outw[1], outw[2], outw[3]));
+            continue;
+          }
+        }
+        // ---- generic f64 path (reference operation order)
+        double b[VEC], x[N][VEC];
+        if (wb) VecIO<DTI>::f64(lds128(sb + v * 16), b);
+        else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) b[e] = 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) VecIO<DTI>::f64(lds128(sb + (i + (wb ? 1 : 0)) * SB + v * 16), x[i]);
+        double y[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          double X[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) X[i] = x[i][e];
+          const uint32_t keep = keep_bits_for<N, VEC>(a, bm, BMB, le, jtensor0 + off + le, e);
+          uint32_t nzm, erm;
+          y[e] = merge_elem_f64<N>(b[e], X, keep, a, c, nzm, erm);
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            cnt_nz[i] += (nzm >> i) & 1u;
+            cnt_er[i] += (erm >> i) & 1u;
+          }
+        }
+        store_vec_f64<DTO, VEC>(g.seg->out, out_base + le, y);
+      }
+      // tail elements (fewer than 16 bytes) straight from global memory
+      for (uint32_t e = main_elems + tid; e < n; e += kCThreads) {
+        const uint64_t idx = g.start + off + e;
+        const double B = wb ? load_f64<DTI>(g.seg->base, idx) : 0.0;
+        double X[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) X[i] = load_f64<DTI>(g.seg->expert[i], idx);
+        uint32_t keep = (1u << N) - 1u;
+        if (a.dropout_mode) {
+          keep = 0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) keep |= (uint32_t)keep_draw(a.seed[i], jtensor0 + off + e, a.thresh) << i;
+        }
+        uint32_t nzm, erm;
+        const double Y = merge_elem_f64<N>(B, X, keep, a, c, nzm, erm);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          cnt_nz[i] += (nzm >> i) & 1u;
+          cnt_er[i] += (erm >> i) & 1u;
+        }
+        store_from_f64<DTO>(g.seg->out, idx, Y);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r.empty[s]);
+      ++q;
+    }
+    // per-item counters -> per-tensor u64 totals (integer atomics: order-independent)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint32_t z = __reduce_add_sync(0xffffffffu, cnt_nz[i]);
+      const uint32_t er = __reduce_add_sync(0xffffffffu, cnt_er[i]);
+      if (lane == 0) {
+        if (z) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + i, (unsigned long long)z);
+        if (er) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + N + i, (unsigned long long)er);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host-side launch helpers
+template <int N>
+static void stage_geometry(int esz, bool bitmap, uint32_t& stage_bytes, uint32_t& nstages) {
+  const uint32_t sb = StreamBytes<N>::v;
+  const uint32_t elems = sb / esz;
+  stage_bytes = (N + 1) * sb + (bitmap ? N * (elems / 8) : 0);
+  stage_bytes = (stage_bytes + 127) & ~127u;
+  nstages = (kSmemBudget - 1024) / stage_bytes;
+  if (nstages > 8) nstages = 8;
+}
+
+template <typename K>
+static int ensure_smem(K kernel, uint32_t bytes) {
+  return cuda_status(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+                     "cudaFuncSetAttribute");
+}
+
+template <int DT, int N>
+static int launch_sumsq(const rlk_fusion_plan& plan, int delta, double* partials, cudaStream_t s) {
+  uint32_t sb, ns;
+  stage_geometry<N>(Elem<DT>::size, false, sb, ns);
+  const uint32_t smem = 1024 + sb * ns;
+  auto kern = k_sumsq<DT, N>;
+  int st = ensure_smem(kern, smem);
+  if (st) return st;
+  uint32_t grid = std::min<uint32_t>(plan.n_items, (uint32_t)sm_count());
+  kern<<<grid, kThreads, smem, s>>>(plan, delta, partials, sb, ns);
+  return launch_status("rlk_fusion_sumsq");
+}
+
+template <int DTI, int DTO, int N>
+static int launch_merge(MergeArgs& a, cudaStream_t s) {
+  uint32_t sb, ns;
+  stage_geometry<N>(Elem<DTI>::size, a.dropout_mode == 2, sb, ns);
+  a.stage_bytes = sb;
+  a.nstages = ns;
+  const uint32_t smem = 1024 + sb * ns;
+  auto kern = k_merge<DTI, DTO, N>;
+  int st = ensure_smem(kern, smem);
+  if (st) return st;
+  uint32_t grid = std::min<uint32_t>(a.plan.n_items, (uint32_t)sm_count());
+  kern<<<grid, kThreads, smem, s>>>(a);
+  return launch_status("rlk_fusion_merge");
+}
+
+template <int DT>
+static int dispatch_sumsq_n(int n, const rlk_fusion_plan& plan, int delta, double* partials, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_sumsq<DT, 1>(plan, delta, partials, s);
+    case 2: return launch_sumsq<DT, 2>(plan, delta, partials, s);
+    case 3: return launch_sumsq<DT, 3>(plan, delta, partials, s);
+    case 4: return launch_sumsq<DT, 4>(plan, delta, partials, s);
+    case 5: return launch_sumsq<DT, 5>(plan, delta, partials, s);
+    case 6: return launch_sumsq<DT, 6>(plan, delta, partials, s);
+    case 7: return launch_sumsq<DT, 7>(plan, delta, partials, s);
+    case 8: return launch_sumsq<DT, 8>(plan, delta, partials, s);
+  }
+  set_error("expert count %d not supported (1..%d)", n, RLK_MAX_EXPERTS);
+  return RLK_ERR_UNSUPPORTED;
+}
+
+template <int DTI, int DTO>
+static int dispatch_merge_n(int n, MergeArgs& a, cudaStream_t s) {
+  switch (n) {
+    case 1: return launch_merge<DTI, DTO, 1>(a, s);
+    case 2: return launch_merge<DTI, DTO, 2>(a, s);
+    case 3: return launch_merge<DTI, DTO, 3>(a, s);
+    case 4: return launch_merge<DTI, DTO, 4>(a, s);
+    case 5: return launch_merge<DTI, DTO, 5>(a, s);
+    case 6: return launch_merge<DTI, DTO, 6>(a, s);
+    case 7: return launch_merge<DTI, DTO, 7>(a, s);
+    case 8: return launch_merge<DTI, DTO, 8>(a, s);
+  }
+  set_error("expert count %d not supported (1..%d)", n, RLK_MAX_EXPERTS);
+  return RLK_ERR_UNSUPPORTED;
+}
+
+template <int DTI>
+static int dispatch_merge_out(int dto, int n, MergeArgs& a, cudaStream_t s) {
+  switch (dto) {
+    case RLK_BF16: return dispatch_merge_n<DTI, RLK_BF16>(n, a, s);
+    case RLK_F32: return dispatch_merge_n<DTI, RLK_F32>(n, a, s);
+    case RLK_F64: return dispatch_merge_n<DTI, RLK_F64>(n, a, s);
+  }
+  set_error("bad output dtype %d", dto);
+  return RLK_ERR_INVALID;
+}
+
+}  // namespace rlk
+
+using namespace rlk;
+
+extern "C" {
+
+int rlk_fusion_sumsq(const rlk_fusion_plan* plan, int n_experts, int dtype, int delta_mode, double* partials,
+                     void* stream) {
+  RLK_REQUIRE(plan != nullptr && partials != nullptr, "rlk_fusion_sumsq: NULL argument");
+  RLK_REQUIRE(n_experts >= 1 && n_experts <= RLK_MAX_EXPERTS, "rlk_fusion_sumsq: bad expert count %d", n_experts);
+  if (plan->n_items == 0) return RLK_OK;
+  RLK_REQUIRE(plan->segs && plan->seg_item_prefix && plan->n_segs > 0, "rlk_fusion_sumsq: empty plan");
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case RLK_BF16: return dispatch_sumsq_n<RLK_BF16>(n_experts, *plan, delta_mode, partials, s);
+    case RLK_F32: return dispatch_sumsq_n<RLK_F32>(n_experts, *plan, delta_mode, partials, s);
+    case RLK_F64: return dispatch_sumsq_n<RLK_F64>(n_experts, *plan, delta_mode, partials, s);
+  }
+  set_error("rlk_fusion_sumsq: bad dtype %d", dtype);
+  return RLK_ERR_INVALID;
+}
+
+int rlk_fusion_finalize(const double* partials, const uint32_t* tensor_items, uint32_t n_tensors, int n_experts,
+                        int target_mode, double target_value, double* sumsq, double* scale, int32_t* status,
+                        void* stream) {
+  RLK_REQUIRE(n_experts >= 1 && n_experts <= RLK_MAX_EXPERTS, "rlk_fusion_finalize: bad expert count %d", n_experts);
+  RLK_REQUIRE(target_mode >= 0 && target_mode <= 2, "rlk_fusion_finalize: bad target mode %d", target_mode);
+  if (n_tensors == 0) return RLK_OK;
+  RLK_REQUIRE(partials && tensor_items && sumsq && scale && status, "rlk_fusion_finalize: NULL argument");
+  const int warps = 8;
+  const uint32_t grid = (n_tensors + warps - 1) / warps;
+  k_finalize<<<grid, warps * 32, 0, (cudaStream_t)stream>>>(partials, tensor_items, n_tensors, n_experts,
+                                                            target_mode, target_value, sumsq, scale, status);
+  return launch_status("rlk_fusion_finalize");
+}
+
+int rlk_fusion_mask_bitmap(const uint64_t* child_seeds, int n_experts, uint64_t thresh, uint64_t n_bits,
+                           uint32_t* bitmap, uint64_t words_per_row, void* stream) {
+  RLK_REQUIRE(n_experts >= 1 && n_experts <= RLK_MAX_EXPERTS, "rlk_fusion_mask_bitmap: bad expert count %d",
+              n_experts);
+  RLK_REQUIRE(child_seeds && bitmap, "rlk_fusion_mask_bitmap: NULL argument");
+  RLK_REQUIRE(words_per_row * 32 >= n_bits, "rlk_fusion_mask_bitmap: row too short");
+  if (n_bits == 0) return RLK_OK;
+  ulonglong4 lo = make_ulonglong4(0, 0, 0, 0), hi = make_ulonglong4(0, 0, 0, 0);
+  for (int i = 0; i < n_experts; ++i) (i < 4 ? (&lo.x)[i] : (&hi.x)[i - 4]) = child_seeds[i];
+  const uint64_t total = ((n_bits + 31) / 32) * (uint64_t)n_experts;
+  const uint64_t blocks = (total + 255) / 256;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(blocks, (uint64_t)sm_count() * 16);
+  k_mask_bitmap<<<grid, 256, 0, (cudaStream_t)stream>>>(lo, hi, n_experts, thresh, n_bits, bitmap, words_per_row);
+  return launch_status("rlk_fusion_mask_bitmap");
+}
+
+int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, int dtype_out, int delta_mode,
+                     const double* scale, const double* weights, int dropout_mode, const uint64_t* child_seeds,
+                     uint64_t thresh, double keep_prob, const uint32_t* bitmap, uint64_t words_per_row,
+                     int erase_mode, unsigned long long* counters, void* stream) {
+  RLK_REQUIRE(plan && scale && weights && counters, "rlk_fusion_merge: NULL argument");
+  RLK_REQUIRE(n_experts >= 1 && n_experts <= RLK_MAX_EXPERTS, "rlk_fusion_merge: bad expert count %d", n_experts);
+  RLK_REQUIRE(dropout_mode >= 0 && dropout_mode <= 2, "rlk_fusion_merge: bad dropout mode %d", dropout_mode);
+  RLK_REQUIRE(erase_mode >= 0 && erase_mode <= 2, "rlk_fusion_merge: bad erase mode %d", erase_mode);
+  RLK_REQUIRE(dropout_mode == 0 || child_seeds, "rlk_fusion_merge: dropout needs child seeds");
+  RLK_REQUIRE(dropout_mode != 2 || (bitmap && words_per_row % 4 == 0),
+              "rlk_fusion_merge: bitmap mode needs a bitmap with 16-byte rows");
+  RLK_REQUIRE(dropout_mode == 0 || (keep_prob > 0.0 && keep_prob <= 1.0), "rlk_fusion_merge: bad keep_prob");
+  if (plan->n_items == 0) return RLK_OK;
+  MergeArgs a;
+  memset(&a, 0, sizeof(a));
+  a.plan = *plan;
+  a.scale = scale;
+  for (int i = 0; i < n_experts; ++i) {
+    a.w[i] = weights[i];
+    a.seed[i] = child_seeds ? child_seeds[i] : 0;
+  }
+  a.thresh = thresh;
+  a.keep_prob = keep_prob;
+  a.inv_keep = 1.0 / keep_prob;
+  a.bitmap = bitmap;
+  a.words_per_row = words_per_row;
+  a.counters = counters;
+  a.dropout_mode = dropout_mode;
+  a.erase_mode = erase_mode;
+  a.delta_mode = delta_mode & 1;
+  a.with_base = (delta_mode & 1) ? ((delta_mode >> 1) & 1) : 1;
+  const char* env = getenv("RLK_MERGE_FAST");
+  a.fast = env ? atoi(env) : 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype_in) {
+    case RLK_BF16: return dispatch_merge_out<RLK_BF16>(dtype_out, n_experts, a, s);
+    case RLK_F32: return dispatch_merge_out<RLK_F32>(dtype_out, n_experts, a, s);
+    case RLK_F64: return dispatch_merge_out<RLK_F64>(dtype_out, n_experts, a, s);
+  }
+  set_error("rlk_fusion_merge: bad input dtype %d", dtype_in);
+  return RLK_ERR_INVALID;
+}
+
+}  // extern "C"

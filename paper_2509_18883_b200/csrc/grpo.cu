@@ -1,0 +1,707 @@
+// GRPO token objective kernels for sm_100a: K4 forward (online log-sum-exp over the vocab row + token
+// gather + TIS + triplet clip epilogue) and K5 backward (coef * (onehot - softmax)).
+//
+// Reference (pkg/src/rolloutlab/):
+//   log_token_dist        toy_env.py:157-175   z / T; lse = max + log(sum(exp(z - max))); z - lse
+//   _triplet_value_slope  objective.py:133-150
+//   tis_weight            objective.py:161-165 min(exp(logp_train - logp_infer), cap)
+//   objective_value       objective.py:230-250 r = exp(logp - logp_train); g_sum += w * value
+//   objective_gradient    objective.py:253-283 coef = norm * w * slope * r / T; row -= coef * p; row[tok] += coef
+//
+// A logits row (V = 131072 bf16 = 256 KiB) is streamed through a TMA bulk-copy ring by one producer
+// lane; eight consumer warps keep a per-thread (max, sum 2^(z*c - max*c)) pair in f32 (c = log2(e) / T,
+// MUFU.EX2 per logit), combined with shuffles at the end of the row.  The epilogue runs in f64.
+#include "common.cuh"
+#include "capi_internal.h"
+#include "pipeline.cuh"
+
+namespace rlk {
+
+constexpr uint32_t kRowStageBytes = 32768;
+constexpr uint32_t kRowStages = 6;
+constexpr double kLog2e = 1.4426950408889634074;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int DT> struct RowVec;
+template <> struct RowVec<RLK_BF16> {
+  static constexpr int n = 8;
+  __device__ static void f32(const uint4& w, float* o) {
+    o[0] = bf16_lo(w.x); o[1] = bf16_hi(w.x); o[2] = bf16_lo(w.y); o[3] = bf16_hi(w.y);
+    o[4] = bf16_lo(w.z); o[5] = bf16_hi(w.z); o[6] = bf16_lo(w.w); o[7] = bf16_hi(w.w);
+  }
+};
+template <> struct RowVec<RLK_F32> {
+  static constexpr int n = 4;
+  __device__ static void f32(const uint4& w, float* o) {
+    o[0] = __uint_as_float(w.x); o[1] = __uint_as_float(w.y); o[2] = __uint_as_float(w.z); o[3] = __uint_as_float(w.w);
+  }
+};
+template <> struct RowVec<RLK_F64> {
+  static constexpr int n = 2;
+  __device__ static void f64(const uint4& w, double* o) {
+    o[0] = __hiloint2double((int)w.y, (int)w.x);
+    o[1] = __hiloint2double((int)w.w, (int)w.z);
+  }
+};
+
+// Producer lane: stream the rows this CTA owns (row = blockIdx.x + k * gridDim.x, skipping inactive
+// rows) through the ring in kRowStageBytes chunks (16-byte multiples; the <16-byte tail is read by
+// consumers from global memory).
+template <typename Active, typename Addr>
+__device__ void produce_rows(const Ring& r, uint64_t n_rows, uint64_t row_bytes, Active active, Addr addr) {
+  const uint64_t pol = policy_evict_first();
+  uint32_t q = 0;
+  for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+    if (!active(row)) continue;
+    const char* src = addr(row);
+    for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
+      const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
+      const uint32_t main_bytes = bytes & ~15u;
+      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      mbar_wait(&r.empty[s], ph ^ 1u);
+      if (main_bytes) {
+        mbar_arrive_expect_tx(&r.full[s], main_bytes);
+        bulk_g2s(r.buf + s * r.stage_bytes, src + off, main_bytes, &r.full[s], pol);
+      } else {
+        mbar_arrive(&r.full[s]);
+      }
+      ++q;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ triplet clip (objective.py:133-150)
+struct TripletOut { double value, slope; };
+__device__ __forceinline__ TripletOut triplet(double r, double adv, const rlk_clip& c) {
+  const double lo = 1.0 - c.eps_neg_low, hi = 1.0 + c.eps_pos_high;
+  const double clipped = fmin(fmax(r, lo), hi);
+  const double clip_slope = (lo <= r && r <= hi) ? 1.0 : 0.0;
+  const double raw = __dmul_rn(r, adv);
+  const double capped = __dmul_rn(clipped, adv);
+  double inner, islope;
+  if (raw <= capped) { inner = raw; islope = adv; }
+  else { inner = capped; islope = __dmul_rn(adv, clip_slope); }
+  if (c.guard_positive && adv > 0.0) return {inner, islope};
+  const double floor_v = __dmul_rn(c.eps_neg_high, adv);
+  if (inner >= floor_v) return {inner, islope};
+  return {floor_v, 0.0};
+}
+
+// log-sum-exp of z / T for a row read straight from global memory (unaligned rows; f64 math).
+template <int DT>
+__device__ double row_lse_global(const char* rowp, uint64_t V, double T, double* red_m, double* red_s) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double m = -INFINITY, sum = 0.0;
+  for (uint64_t v = threadIdx.x; v < V; v += kCThreads) {
+    const double z = load_f64<DT>(rowp, v);
+    const double zt = T == 1.0 ? z : __ddiv_rn(z, T);
+    if (zt > m) { sum = sum * exp(m - zt); m = zt; }
+    sum += exp(zt - m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
+    const double M = fmax(m, om);
+    sum = (M == -INFINITY) ? 0.0 : sum * exp(m - M) + os * exp(om - M);
+    m = M;
+  }
+  if (lane == 0) { red_m[warp] = m; red_s[warp] = sum; }
+  cbar_sync();
+  double M = red_m[0];
+  for (int w = 1; w < kCWarps; ++w) M = fmax(M, red_m[w]);
+  double S = 0.0;
+  for (int w = 0; w < kCWarps; ++w) S += red_m[w] == -INFINITY ? 0.0 : red_s[w] * exp(red_m[w] - M);
+  cbar_sync();
+  return M + log(S);
+}
+
+struct FwdArgs {
+  const char* logits;
+  uint64_t n_rows, vocab, row_stride;
+  const int64_t* row_index;
+  const int32_t* tokens;
+  const double* lp_train;
+  const double* lp_infer;
+  const int32_t* sample;
+  const double* adv;
+  const uint8_t* use;
+  const double* temp;
+  const double* norm;
+  rlk_clip clip;
+  double *logp, *lse, *term, *coef;
+  int32_t* flags;
+};
+
+// f64 epilogue for one token given its natural-log lse (thread-level).
+template <int DT>
+__device__ void fwd_epilogue(const FwdArgs& a, uint64_t row, const char* rowp, double lse) {
+  const int32_t s = a.sample[row];
+  const double T = a.temp[s];
+  const int32_t tok = a.tokens[row];
+  if (tok < 0 || (uint64_t)tok >= a.vocab) {
+    atomicOr(a.flags, 2);
+    if (a.logp) a.logp[row] = nan("");
+    if (a.lse) a.lse[row] = lse;
+    a.term[row] = 0.0;
+    a.coef[row] = 0.0;
+    return;
+  }
+  const double z = load_f64<DT>(rowp, (uint64_t)tok);
+  const double zt = (T == 1.0) ? z : __ddiv_rn(z, T);  // toy_env.py:168-171
+  const double logp = __dsub_rn(zt, lse);
+  const double lt = a.lp_train[row], li = a.lp_infer[row];
+  const double r = exp(__dsub_rn(logp, lt));                                // objective.py:245
+  const double w = fmin(exp(__dsub_rn(lt, li)), a.clip.tis_cap);           // objective.py:161-165
+  const TripletOut tv = triplet(r, a.adv[s], a.clip);                       // objective.py:247
+  if (!isfinite(logp)) atomicOr(a.flags, 1);
+  if (a.logp) a.logp[row] = logp;
+  if (a.lse) a.lse[row] = lse;
+  a.term[row] = __dmul_rn(w, tv.value);
+  // objective.py:279: coef = norm * w * slope * r_theta / tau (left to right)
+  a.coef[row] = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(a.norm[s], w), tv.slope), r), T);
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int ESZ = Elem<DT>::size;
+  constexpr int VEC = 16 / ESZ;
+  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages);
+  const uint64_t row_bytes = a.vocab * ESZ;
+  auto active = [&](uint64_t row) { return a.use[a.sample[row]] != 0; };
+  auto addr = [&](uint64_t row) {
+    const uint64_t rr = a.row_index ? (uint64_t)a.row_index[row] : row;
+    return a.logits + rr * a.row_stride * ESZ;
+  };
+  // rows whose start is not 16-byte aligned (tiny toy vocabularies) bypass the TMA ring
+  auto streamed = [&](uint64_t row) { return active(row) && ((uintptr_t)addr(row) & 15u) == 0; };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  if (warp == kCWarps) {
+    if (lane == 0) produce_rows(r, a.n_rows, row_bytes, streamed, addr);
+    return;
+  }
+  __shared__ double red_m[kCWarps], red_s[kCWarps];
+  uint32_t q = 0;
+  for (uint64_t row = blockIdx.x; row < a.n_rows; row += gridDim.x) {
+    if (!active(row)) {
+      if (tid == 0) {
+        if (a.logp) a.logp[row] = 0.0;
+        if (a.lse) a.lse[row] = 0.0;
+        a.term[row] = 0.0;
+        a.coef[row] = 0.0;
+      }
+      continue;
+    }
+    const char* rowp = addr(row);
+    const double T = a.temp[a.sample[row]];
+    double lse;
+    if (((uintptr_t)rowp & 15u) != 0) {
+      lse = row_lse_global<DT>(rowp, a.vocab, T, red_m, red_s);
+    } else if constexpr (DT == RLK_F64) {
+      // f64 path: online max / sum of exp(z/T - m) with exact division (toy_env.py:168-174)
+      double m = -INFINITY, sum = 0.0;
+      for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
+        const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
+        const uint32_t main_bytes = bytes & ~15u;
+        const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+        mbar_wait(&r.full[s], ph);
+        const uint8_t* sb = r.buf + s * r.stage_bytes;
+        for (uint32_t v = tid; v < main_bytes / 16; v += kCThreads) {
+          double z[2];
+          RowVec<RLK_F64>::f64(lds128(sb + v * 16), z);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double zt = T == 1.0 ? z[e] : __ddiv_rn(z[e], T);
+            if (zt > m) { sum = sum * exp(m - zt); m = zt; }
+            sum += exp(zt - m);
+          }
+        }
+        for (uint32_t e = main_bytes / 8 + tid; e < bytes / 8; e += kCThreads) {
+          const double z = load_f64<DT>(rowp, off / 8 + e);
+          const double zt = T == 1.0 ? z : __ddiv_rn(z, T);
+          if (zt > m) { sum = sum * exp(m - zt); m = zt; }
+          sum += exp(zt - m);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&r.empty[s]);
+        ++q;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
+        const double M = fmax(m, om);
+        sum = (M == -INFINITY) ? 0.0 : sum * exp(m - M) + os * exp(om - M);
+        m = M;
+      }
+      if (lane == 0) { red_m[warp] = m; red_s[warp] = sum; }
+      cbar_sync();
+      double M = red_m[0];
+      for (int w = 1; w < kCWarps; ++w) M = fmax(M, red_m[w]);
+      double S = 0.0;
+      for (int w = 0; w < kCWarps; ++w) S += red_m[w] == -INFINITY ? 0.0 : red_s[w] * exp(red_m[w] - M);
+      lse = M + log(S);
+      cbar_sync();
+    } else {
+      // f32 path in the log2 domain: x = z * c, c = log2(e) / T; one MUFU.EX2 per logit.
+      const float c = (float)(kLog2e / T);
+      float mz = -INFINITY, sum = 0.f, nb = INFINITY;
+      for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
+        const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
+        const uint32_t main_bytes = bytes & ~15u;
+        const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+        mbar_wait(&r.full[s], ph);
+        const uint8_t* sb = r.buf + s * r.stage_bytes;
+        const uint32_t nvec = main_bytes / 16;
+        for (uint32_t v = tid; v < nvec; v += kCThreads) {
+          float z[VEC];
+          RowVec<DT>::f32(lds128(sb + v * 16), z);
+          float lm = z[0];
+#pragma unroll
+          for (int e = 1; e < VEC; ++e) lm = fmaxf(lm, z[e]);
+          if (lm > mz) {
+            sum *= ex2_approx((mz - lm) * c);
+            mz = lm;
+            nb = -mz * c;
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) sum += ex2_approx(fmaf(z[e], c, nb));
+        }
+        for (uint32_t e = main_bytes / ESZ + tid; e < bytes / ESZ; e += kCThreads) {
+          const float z = (float)load_f64<DT>(rowp, off / ESZ + e);
+          if (z > mz) {
+            sum *= ex2_approx((mz - z) * c);
+            mz = z;
+            nb = -mz * c;
+          }
+          sum += ex2_approx(fmaf(z, c, nb));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&r.empty[s]);
+        ++q;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, mz, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float M = fmaxf(mz, om);
+        sum = (M == -INFINITY) ? 0.f : sum * ex2_approx((mz - M) * c) + os * ex2_approx((om - M) * c);
+        mz = M;
+      }
+      if (lane == 0) { red_m[warp] = mz; red_s[warp] = sum; }
+      cbar_sync();
+      double M = red_m[0];
+      for (int w = 1; w < kCWarps; ++w) M = fmax(M, red_m[w]);
+      double S = 0.0;
+      for (int w = 0; w < kCWarps; ++w)
+        S += red_m[w] == -INFINITY ? 0.0 : red_s[w] * exp2((red_m[w] - M) * (kLog2e / T));
+      // lse of z/T (natural log): max/T + ln(S)
+      lse = (T == 1.0 ? M : M / T) + log(S);
+      cbar_sync();
+    }
+    if (tid == 0) fwd_epilogue<DT>(a, row, rowp, lse);
+  }
+}
+
+// ------------------------------------------------------------------ K5 backward
+struct BwdArgs {
+  const char* logits;
+  uint64_t n_out_rows, vocab, row_stride;
+  const int64_t* logits_row;
+  const int64_t* row_tok_ptr;
+  const int64_t* row_tok;
+  const int32_t* tokens;
+  const double* temp;
+  const double* lse;
+  const double* coef;
+  char* grad;
+  uint64_t grad_row_stride;
+};
+
+__device__ __forceinline__ void tok_range(const BwdArgs& a, uint64_t o, int64_t& k0, int64_t& k1) {
+  if (a.row_tok_ptr) { k0 = a.row_tok_ptr[o]; k1 = a.row_tok_ptr[o + 1]; }
+  else { k0 = (int64_t)o; k1 = (int64_t)o + 1; }
+}
+__device__ __forceinline__ int64_t tok_at(const BwdArgs& a, int64_t k) { return a.row_tok ? a.row_tok[k] : k; }
+
+template <int GT>
+__device__ __forceinline__ void store_grad_f32(char* g, uint64_t idx, const float* v, int n) {
+  if constexpr (GT == RLK_BF16) {
+    if (n == 8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+        w[e] = *reinterpret_cast<uint32_t*>(&p);
+      }
+      stg128_stream((uint16_t*)g + idx, make_uint4(w[0], w[1], w[2], w[3]));
+    } else {
+      for (int e = 0; e < n; ++e) reinterpret_cast<uint16_t*>(g)[idx + e] = f32_to_bf16_rne(v[e]);
+    }
+  } else if constexpr (GT == RLK_F32) {
+    if (n % 4 == 0) {
+      for (int e = 0; e < n; e += 4)
+        stg128_stream((float*)g + idx + e, make_uint4(__float_as_uint(v[e]), __float_as_uint(v[e + 1]),
+                                                       __float_as_uint(v[e + 2]), __float_as_uint(v[e + 3])));
+    } else {
+      for (int e = 0; e < n; ++e) reinterpret_cast<float*>(g)[idx + e] = v[e];
+    }
+  } else {
+    for (int e = 0; e < n; ++e) reinterpret_cast<double*>(g)[idx + e] = (double)v[e];
+  }
+}
+
+template <int DT, int GT>
+__global__ void __launch_bounds__(kThreads, 1) k_grpo_bwd(BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int ESZ = Elem<DT>::size;
+  constexpr int GSZ = Elem<GT>::size;
+  constexpr int VEC = 16 / ESZ;
+  constexpr bool F64MATH = (DT == RLK_F64) || (GT == RLK_F64);
+  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages);
+  const uint64_t row_bytes = a.vocab * ESZ;
+  auto lrow = [&](uint64_t o) { return a.logits_row ? (uint64_t)a.logits_row[o] : o; };
+  auto active = [&](uint64_t o) {
+    int64_t k0, k1;
+    tok_range(a, o, k0, k1);
+    for (int64_t k = k0; k < k1; ++k)
+      if (a.coef[tok_at(a, k)] != 0.0) return true;
+    return false;
+  };
+  auto addr = [&](uint64_t o) { return a.logits + lrow(o) * a.row_stride * ESZ; };
+  auto streamed = [&](uint64_t o) { return active(o) && ((uintptr_t)addr(o) & 15u) == 0; };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  if (warp == kCWarps) {
+    if (lane == 0) produce_rows(r, a.n_out_rows, row_bytes, streamed, addr);
+    return;
+  }
+  uint32_t q = 0;
+  for (uint64_t o = blockIdx.x; o < a.n_out_rows; o += gridDim.x) {
+    char* grow = a.grad + lrow(o) * a.grad_row_stride * GSZ;
+    if (!active(o)) {
+      // objective.py:275-276 leaves the row at zero
+      const uint64_t gbytes = a.vocab * GSZ;
+      if (((uintptr_t)grow & 15u) == 0) {
+        for (uint64_t b = (uint64_t)tid * 16; b + 16 <= gbytes; b += kCThreads * 16)
+          stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
+        for (uint64_t b = (gbytes & ~15ull) + tid; b < gbytes; b += kCThreads) grow[b] = 0;
+      } else {
+        for (uint64_t b = tid; b < gbytes; b += kCThreads) grow[b] = 0;
+      }
+      continue;
+    }
+    int64_t k0, k1;
+    tok_range(a, o, k0, k1);
+    const char* rowp = addr(o);
+    if (((uintptr_t)rowp & 15u) != 0 || ((uintptr_t)grow & 15u) != 0) {
+      // unaligned row: reference-order f64 evaluation straight from global memory
+      for (uint64_t v = tid; v < a.vocab; v += kCThreads) {
+        const double z = load_f64<DT>(rowp, v);
+        double g = 0.0;
+        for (int64_t k = k0; k < k1; ++k) {
+          const int64_t t = tok_at(a, k);
+          const double cf = a.coef[t];
+          if (cf == 0.0) continue;
+          const double T = a.temp[t];
+          const double p = exp(__dsub_rn(T == 1.0 ? z : __ddiv_rn(z, T), a.lse[t]));
+          g = __dsub_rn(g, __dmul_rn(cf, p));
+          if ((int64_t)v == (int64_t)a.tokens[t]) g = __dadd_rn(g, cf);
+        }
+        store_from_f64<GT>(grow, v, g);
+      }
+      continue;
+    }
+    for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
+      const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
+      const uint32_t main_bytes = bytes & ~15u;
+      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      mbar_wait(&r.full[s], ph);
+      const uint8_t* sb = r.buf + s * r.stage_bytes;
+      const uint64_t v0 = off / ESZ;  // first vocab index of this stage
+      const uint32_t nvec = main_bytes / 16;
+      for (uint32_t v = tid; v < nvec + ((bytes - main_bytes) ? 1u : 0u); v += kCThreads) {
+        const bool tail = v >= nvec;
+        const int n = tail ? (int)((bytes - main_bytes) / ESZ) : VEC;
+        const uint64_t vb = v0 + (uint64_t)v * VEC;
+        if constexpr (F64MATH) {
+          double z[VEC], g[VEC];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            z[e] = 0.0;
+            g[e] = 0.0;
+          }
+          if (!tail) {
+            if constexpr (DT == RLK_F64) RowVec<RLK_F64>::f64(lds128(sb + v * 16), z);
+            else {
+              float zf[VEC];
+              RowVec<DT>::f32(lds128(sb + v * 16), zf);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) z[e] = zf[e];
+            }
+          } else {
+            for (int e = 0; e < n; ++e) z[e] = load_f64<DT>(rowp, vb + e);
+          }
+          for (int64_t k = k0; k < k1; ++k) {
+            const int64_t t = tok_at(a, k);
+            const double cf = a.coef[t];
+            if (cf == 0.0) continue;
+            const double T = a.temp[t], L = a.lse[t];
+            const int64_t tk = a.tokens[t];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              const double zt = T == 1.0 ? z[e] : __ddiv_rn(z[e], T);
+              const double p = exp(__dsub_rn(zt, L));
+              g[e] = __dsub_rn(g[e], __dmul_rn(cf, p));
+              if ((int64_t)(vb + e) == tk) g[e] = __dadd_rn(g[e], cf);
+            }
+          }
+          for (int e = 0; e < n; ++e) store_from_f64<GT>(grow, vb + e, g[e]);
+        } else {
+          float z[VEC], g[VEC];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            z[e] = 0.f;
+            g[e] = 0.f;
+          }
+          if (!tail) RowVec<DT>::f32(lds128(sb + v * 16), z);
+          else
+            for (int e = 0; e < n; ++e) z[e] = (float)load_f64<DT>(rowp, vb + e);
+          for (int64_t k = k0; k < k1; ++k) {
+            const int64_t t = tok_at(a, k);
+            const double cfd = a.coef[t];
+            if (cfd == 0.0) continue;
+            const double T = a.temp[t];
+            const float c = (float)(kLog2e / T), nl = (float)(-a.lse[t] * kLog2e), cf = (float)cfd;
+            const int64_t tk = a.tokens[t];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              g[e] = fmaf(-cf, ex2_approx(fmaf(z[e], c, nl)), g[e]);
+              if ((int64_t)(vb + e) == tk) g[e] += cf;
+            }
+          }
+          store_grad_f32<GT>(grow, vb, g, n);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r.empty[s]);
+      ++q;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ log_token_dist rows (f64 math)
+template <int DT, int OT>
+__global__ void k_logsoftmax_rows(const char* logits, uint64_t n_rows, uint64_t vocab, uint64_t row_stride,
+                                  const int64_t* row_index, const double* temp, char* out) {
+  constexpr int ESZ = Elem<DT>::size;
+  __shared__ double red_m[32], red_s[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+    const uint64_t rr = row_index ? (uint64_t)row_index[row] : row;
+    const char* rowp = logits + rr * row_stride * ESZ;
+    const double T = temp[row];
+    double m = -INFINITY;
+    for (uint64_t v = threadIdx.x; v < vocab; v += blockDim.x) {
+      const double z = load_f64<DT>(rowp, v);
+      m = fmax(m, T == 1.0 ? z : __ddiv_rn(z, T));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red_m[warp] = m;
+    __syncthreads();
+    double M = red_m[0];
+    for (int w = 1; w < nw; ++w) M = fmax(M, red_m[w]);
+    double s = 0.0;
+    for (uint64_t v = threadIdx.x; v < vocab; v += blockDim.x) {
+      const double z = load_f64<DT>(rowp, v);
+      s += exp(__dsub_rn(T == 1.0 ? z : __ddiv_rn(z, T), M));
+    }
+    s = warp_sum_f64(s);
+    if (lane == 0) red_s[warp] = s;
+    __syncthreads();
+    double S = 0.0;
+    for (int w = 0; w < nw; ++w) S += red_s[w];
+    const double lse = M + log(S);  // toy_env.py:172-174
+    for (uint64_t v = threadIdx.x; v < vocab; v += blockDim.x) {
+      const double z = load_f64<DT>(rowp, v);
+      store_from_f64<OT>(out, row * vocab + v, __dsub_rn(T == 1.0 ? z : __ddiv_rn(z, T), lse));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_segment_sum(const double* __restrict__ x, const int64_t* __restrict__ seg, uint64_t n_segs,
+                              double* __restrict__ out) {
+  const uint64_t g = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= n_segs) return;
+  double acc = 0.0;
+  for (int64_t i = seg[g] + lane; i < seg[g + 1]; i += 32) acc += x[i];
+  acc = warp_sum_f64(acc);
+  if (lane == 0) out[g] = acc;
+}
+
+static int grid_rows(uint64_t n_rows) {
+  const uint64_t sms = (uint64_t)sm_count();
+  return (int)(n_rows < sms ? n_rows : sms);
+}
+
+template <typename K>
+static int set_smem(K kern, uint32_t bytes) {
+  return cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes),
+                     "cudaFuncSetAttribute");
+}
+
+template <int DT>
+static int launch_fwd(const FwdArgs& a, cudaStream_t s) {
+  const uint32_t smem = 1024 + kRowStageBytes * kRowStages;
+  auto kern = k_grpo_fwd<DT>;
+  if (int st = set_smem(kern, smem)) return st;
+  kern<<<grid_rows(a.n_rows), kThreads, smem, s>>>(a);
+  return launch_status("rlk_grpo_fwd");
+}
+
+template <int DT, int GT>
+static int launch_bwd(const BwdArgs& a, cudaStream_t s) {
+  const uint32_t smem = 1024 + kRowStageBytes * kRowStages;
+  auto kern = k_grpo_bwd<DT, GT>;
+  if (int st = set_smem(kern, smem)) return st;
+  kern<<<grid_rows(a.n_out_rows), kThreads, smem, s>>>(a);
+  return launch_status("rlk_grpo_bwd");
+}
+
+template <int DT>
+static int dispatch_bwd(int gt, const BwdArgs& a, cudaStream_t s) {
+  switch (gt) {
+    case RLK_BF16: return launch_bwd<DT, RLK_BF16>(a, s);
+    case RLK_F32: return launch_bwd<DT, RLK_F32>(a, s);
+    case RLK_F64: return launch_bwd<DT, RLK_F64>(a, s);
+  }
+  set_error("rlk_grpo_bwd: bad grad dtype %d", gt);
+  return RLK_ERR_INVALID;
+}
+
+template <int DT>
+static int dispatch_lsm(int ot, const char* lg, uint64_t n, uint64_t V, uint64_t st, const int64_t* ri,
+                        const double* T, char* out, cudaStream_t s) {
+  const int grid = grid_rows(n) * 4;
+  switch (ot) {
+    case RLK_BF16: k_logsoftmax_rows<DT, RLK_BF16><<<grid, 256, 0, s>>>(lg, n, V, st, ri, T, out); break;
+    case RLK_F32: k_logsoftmax_rows<DT, RLK_F32><<<grid, 256, 0, s>>>(lg, n, V, st, ri, T, out); break;
+    case RLK_F64: k_logsoftmax_rows<DT, RLK_F64><<<grid, 256, 0, s>>>(lg, n, V, st, ri, T, out); break;
+    default: set_error("rlk_logsoftmax_rows: bad out dtype %d", ot); return RLK_ERR_INVALID;
+  }
+  return launch_status("rlk_logsoftmax_rows");
+}
+
+
+}  // namespace rlk
+
+using namespace rlk;
+
+extern "C" {
+
+int rlk_grpo_fwd(const void* logits, int dtype, uint64_t n_rows, uint64_t vocab, uint64_t row_stride,
+                 const int64_t* row_index, const int32_t* tokens, const double* logp_train, const double* logp_infer,
+                 const int32_t* sample_of_row, const double* adv, const uint8_t* use, const double* temperature,
+                 const double* norm, const rlk_clip* clip, double* logp_out, double* lse_out, double* term,
+                 double* coef, int32_t* flags, void* stream) {
+  if (n_rows == 0) return RLK_OK;
+  RLK_REQUIRE(logits && tokens && logp_train && logp_infer && sample_of_row && adv && use && temperature && norm &&
+                  clip && term && coef && flags,
+              "rlk_grpo_fwd: NULL argument");
+  RLK_REQUIRE(vocab >= 1 && row_stride >= vocab, "rlk_grpo_fwd: bad vocab/row_stride");
+  RLK_REQUIRE(dtype >= RLK_BF16 && dtype <= RLK_F64, "rlk_grpo_fwd: bad dtype %d", dtype);
+  const int esz = dtype == RLK_BF16 ? 2 : (dtype == RLK_F32 ? 4 : 8);
+  RLK_REQUIRE(((uintptr_t)logits % esz) == 0, "rlk_grpo_fwd: logits must be element-aligned");
+  FwdArgs a;
+  a.logits = (const char*)logits;
+  a.n_rows = n_rows;
+  a.vocab = vocab;
+  a.row_stride = row_stride;
+  a.row_index = row_index;
+  a.tokens = tokens;
+  a.lp_train = logp_train;
+  a.lp_infer = logp_infer;
+  a.sample = sample_of_row;
+  a.adv = adv;
+  a.use = use;
+  a.temp = temperature;
+  a.norm = norm;
+  a.clip = *clip;
+  a.logp = logp_out;
+  a.lse = lse_out;
+  a.term = term;
+  a.coef = coef;
+  a.flags = flags;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case RLK_BF16: return launch_fwd<RLK_BF16>(a, s);
+    case RLK_F32: return launch_fwd<RLK_F32>(a, s);
+    default: return launch_fwd<RLK_F64>(a, s);
+  }
+}
+
+int rlk_segment_sum_f64(const double* x, const int64_t* seg_ptr, uint64_t n_segs, double* out, void* stream) {
+  if (n_segs == 0) return RLK_OK;
+  RLK_REQUIRE(x && seg_ptr && out, "rlk_segment_sum_f64: NULL argument");
+  const uint64_t grid = (n_segs + 7) / 8;
+  k_segment_sum<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(x, seg_ptr, n_segs, out);
+  return launch_status("rlk_segment_sum_f64");
+}
+
+int rlk_grpo_bwd(const void* logits, int dtype, uint64_t n_out_rows, uint64_t vocab, uint64_t row_stride,
+                 const int64_t* logits_row, const int64_t* row_tok_ptr, const int64_t* row_tok, const int32_t* tokens,
+                 const double* temperature_tok, const double* lse, const double* coef, void* grad, int grad_dtype,
+                 uint64_t grad_row_stride, void* stream) {
+  if (n_out_rows == 0) return RLK_OK;
+  RLK_REQUIRE(logits && tokens && temperature_tok && lse && coef && grad, "rlk_grpo_bwd: NULL argument");
+  RLK_REQUIRE(vocab >= 1 && row_stride >= vocab && grad_row_stride >= vocab, "rlk_grpo_bwd: bad strides");
+  RLK_REQUIRE(dtype >= RLK_BF16 && dtype <= RLK_F64, "rlk_grpo_bwd: bad dtype %d", dtype);
+  const int esz = dtype == RLK_BF16 ? 2 : (dtype == RLK_F32 ? 4 : 8);
+  const int gsz = grad_dtype == RLK_BF16 ? 2 : (grad_dtype == RLK_F32 ? 4 : 8);
+  RLK_REQUIRE(((uintptr_t)logits % esz) == 0 && ((uintptr_t)grad % gsz) == 0,
+              "rlk_grpo_bwd: logits / grad must be element-aligned");
+  BwdArgs a;
+  a.logits = (const char*)logits;
+  a.n_out_rows = n_out_rows;
+  a.vocab = vocab;
+  a.row_stride = row_stride;
+  a.logits_row = logits_row;
+  a.row_tok_ptr = row_tok_ptr;
+  a.row_tok = row_tok;
+  a.tokens = tokens;
+  a.temp = temperature_tok;
+  a.lse = lse;
+  a.coef = coef;
+  a.grad = (char*)grad;
+  a.grad_row_stride = grad_row_stride;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case RLK_BF16: return dispatch_bwd<RLK_BF16>(grad_dtype, a, s);
+    case RLK_F32: return dispatch_bwd<RLK_F32>(grad_dtype, a, s);
+    default: return dispatch_bwd<RLK_F64>(grad_dtype, a, s);
+  }
+}
+
+int rlk_logsoftmax_rows(const void* logits, int dtype, uint64_t n_rows, uint64_t vocab, uint64_t row_stride,
+                        const int64_t* row_index, const double* temperature_row, void* out, int out_dtype,
+                        void* stream) {
+  if (n_rows == 0) return RLK_OK;
+  RLK_REQUIRE(logits && temperature_row && out, "rlk_logsoftmax_rows: NULL argument");
+  RLK_REQUIRE(vocab >= 1 && row_stride >= vocab, "rlk_logsoftmax_rows: bad vocab/row_stride");
+  cudaStream_t s = (cudaStream_t)stream;
+  const char* lg = (const char*)logits;
+  switch (dtype) {
+    case RLK_BF16: return dispatch_lsm<RLK_BF16>(out_dtype, lg, n_rows, vocab, row_stride, row_index, temperature_row, (char*)out, s);
+    case RLK_F32: return dispatch_lsm<RLK_F32>(out_dtype, lg, n_rows, vocab, row_stride, row_index, temperature_row, (char*)out, s);
+    case RLK_F64: return dispatch_lsm<RLK_F64>(out_dtype, lg, n_rows, vocab, row_stride, row_index, temperature_row, (char*)out, s);
+  }
+  set_error("rlk_logsoftmax_rows: bad dtype %d", dtype);
+  return RLK_ERR_INVALID;
+}
+
+}  // extern "C"

@@ -1,0 +1,443 @@
+"""GRPO token-level objective on B200 (drop-in for `rolloutlab.objective`).
+
+Reference: pkg/src/rolloutlab/objective.py.  The per-token term is
+
+    min(exp(logp_train - logp_infer), cap) * triplet_clip(exp(logp - logp_train), A)
+
+summed over the USE samples of each group, divided by G * T_max, averaged over groups
+(objective.py:230-250).  The vocab-wide work -- log-softmax of z / T, the gather of the token's
+log-prob, the ratio / TIS / clip epilogue and the gradient coef * (onehot - softmax) -- runs in the
+sm_100a kernels of csrc/grpo.cu (K4 `rlk_grpo_fwd`, K5 `rlk_grpo_bwd`).  Advantages, masks and the
+batch packing are host logic, as in the reference.
+
+Two entry points:
+* the reference's object API (`objective_value`, `objective_gradient` over `MaskedBatch` +
+  `ParamTable`), packed into the tensor form;
+* the tensor API `grpo_token_objective` / `GRPOTokenLoss` over packed logits rows [R, V] (the LLM
+  layout: one row per response token) -- the hot path benchmarked in bench.py.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from enum import Enum
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .core import Group, RewardKind, Sample, SampleStatus
+from .toy_env import ParamTable, detect_repetition
+
+
+# ----------------------------------------------------------------------------- configs / records
+@dataclass(frozen=True)
+class ClipConfig:
+    """Triplet clip + TIS cap, validated like objective.py:40-58."""
+
+    eps_neg_low: float = 0.2
+    eps_pos_high: float = 0.2
+    eps_neg_high: float = 3.0
+    tis_cap: float = 2.0
+    guard_positive: bool = True
+
+    def __post_init__(self):
+        if not 0.0 < self.eps_neg_low < 1.0:
+            raise ValueError("eps_neg_low must be in (0, 1)")
+        if self.eps_pos_high <= 0.0:
+            raise ValueError("eps_pos_high must be > 0")
+        if self.eps_neg_high <= 1.0:
+            raise ValueError("eps_neg_high must be > 1")
+        if self.eps_neg_high < 1.0 + self.eps_pos_high:
+            raise ValueError("eps_neg_high must be >= 1 + eps_pos_high")
+        if self.tis_cap < 1.0:
+            raise ValueError("tis_cap must be >= 1")
+
+    def c_struct(self) -> L.ClipC:
+        return L.ClipC(self.eps_neg_low, self.eps_pos_high, self.eps_neg_high, self.tis_cap,
+                       1 if self.guard_positive else 0)
+
+
+class NormMode(Enum):
+    MEAN_STD = "mean_std"
+    MEAN_ONLY = "mean_only"
+
+
+@dataclass(frozen=True)
+class AdvantageConfig:
+    norm_mode: NormMode = NormMode.MEAN_STD
+    std_floor: float = 1e-8
+
+    def __post_init__(self):
+        if self.std_floor <= 0.0:
+            raise ValueError("std_floor must be > 0")
+
+
+class Mask(Enum):
+    USE = "use"
+    MASK_GRADE_ERROR = "mask_grade_error"
+    MASK_TRUNCATED = "mask_truncated"
+
+
+@dataclass(frozen=True)
+class RepetitionConfig:
+    ngram: int = 2
+    min_repeats: int = 3
+
+
+@dataclass(frozen=True)
+class MaskedGroup:
+    group: Group
+    advantages: tuple[float, ...]
+    masks: tuple[Mask, ...]
+
+    def __post_init__(self):
+        if not (len(self.advantages) == len(self.masks) == self.group.size):
+            raise ValueError("advantages/masks must align with the group's samples")
+
+
+@dataclass(frozen=True)
+class MaskedBatch:
+    groups: tuple[MaskedGroup, ...]
+    t_max: int
+
+    def __post_init__(self):
+        if self.t_max < 1:
+            raise ValueError("t_max must be >= 1")
+        longest = max((len(s.tokens) for mg in self.groups for s in mg.group.samples), default=0)
+        if self.t_max < longest:
+            raise ValueError(f"t_max {self.t_max} below max token length {longest}")
+        if len({mg.group.size for mg in self.groups}) > 1:
+            raise ValueError("all groups in a batch must share the same G")
+
+
+# ----------------------------------------------------------------------------- host scalar math
+def group_advantages(rewards: Sequence[float], cfg: AdvantageConfig) -> list[float]:
+    """(r - mean) / max(population std, floor), or r - mean (objective.py:119-130)."""
+    if len(rewards) < 2:
+        raise ValueError("advantage normalization needs G >= 2 rewards")
+    r = np.asarray(rewards, dtype=np.float64)
+    if not np.isfinite(r).all():
+        raise ValueError("rewards must be finite")
+    centred = r - r.mean()
+    if cfg.norm_mode is NormMode.MEAN_ONLY:
+        return [float(x) for x in centred]
+    denom = max(float(r.std()), cfg.std_floor)
+    return [float(x / denom) for x in centred]
+
+
+def _triplet_value_slope(r_theta: float, adv: float, cfg: ClipConfig) -> tuple[float, float]:
+    """Host copy of the kernel's triplet epilogue (objective.py:133-150); ties take the unclipped branch."""
+    lo, hi = 1.0 - cfg.eps_neg_low, 1.0 + cfg.eps_pos_high
+    clipped = min(max(r_theta, lo), hi)
+    in_band = 1.0 if lo <= r_theta <= hi else 0.0
+    raw, capped = r_theta * adv, clipped * adv
+    inner, slope = (raw, adv) if raw <= capped else (capped, adv * in_band)
+    if cfg.guard_positive and adv > 0.0:
+        return inner, slope
+    floor = cfg.eps_neg_high * adv
+    return (inner, slope) if inner >= floor else (floor, 0.0)
+
+
+def triplet_clip_term(r_theta: float, adv: float, cfg: ClipConfig) -> float:
+    if r_theta <= 0.0:
+        raise ValueError("probability ratio must be > 0")
+    return _triplet_value_slope(r_theta, adv, cfg)[0]
+
+
+def tis_weight(logp_mu_train: float, logp_mu_infer: float, cap: float) -> float:
+    """min(exp(logp_train - logp_infer), cap) (objective.py:161-165)."""
+    if not (math.isfinite(logp_mu_train) and math.isfinite(logp_mu_infer)):
+        raise ValueError("log-probs must be finite")
+    return min(math.exp(logp_mu_train - logp_mu_infer), cap)
+
+
+def apply_masks(groups: Sequence[Group], t_max: int, rep_cfg: RepetitionConfig = RepetitionConfig(),
+                adv_cfg: AdvantageConfig = AdvantageConfig()) -> MaskedBatch:
+    """Mask GradeErrors and non-repetitive truncations; advantages over usable samples (objective.py:168-203)."""
+    out = []
+    for group in groups:
+        masks = []
+        for s in group.samples:
+            if s.reward is None:
+                raise ValueError(f"ungraded sample for prompt {s.prompt_id}")
+            if s.reward.kind is RewardKind.GRADE_ERROR:
+                masks.append(Mask.MASK_GRADE_ERROR)
+            elif s.status is SampleStatus.TRUNCATED and not detect_repetition(s.tokens, rep_cfg.ngram,
+                                                                                rep_cfg.min_repeats):
+                masks.append(Mask.MASK_TRUNCATED)
+            else:
+                masks.append(Mask.USE)
+        usable = [i for i, m in enumerate(masks) if m is Mask.USE]
+        adv = [0.0] * group.size
+        if len(usable) >= 2:
+            for i, a in zip(usable, group_advantages([group.samples[i].reward.raw_score for i in usable], adv_cfg)):
+                adv[i] = a
+        out.append(MaskedGroup(group, tuple(adv), tuple(masks)))
+    return MaskedBatch(tuple(out), t_max)
+
+
+# ----------------------------------------------------------------------------- tensor API
+@dataclass
+class GRPOBatch:
+    """Packed device-side description of a token batch (rows grouped by sample, samples by group).
+
+    sample_of_row[R] i32, tokens[R] i32, logp_train/logp_infer[R] f64, row_index[R] i64 or None,
+    per sample: adv, use (u8), temperature, norm = 1/(n_groups*G*T_max); group_rows[n_groups+1] i64."""
+
+    tokens: torch.Tensor
+    logp_train: torch.Tensor
+    logp_infer: torch.Tensor
+    sample_of_row: torch.Tensor
+    adv: torch.Tensor
+    use: torch.Tensor
+    temperature: torch.Tensor
+    norm: torch.Tensor
+    group_rows: torch.Tensor
+    n_groups: int
+    group_size: int
+    t_max: int
+    row_index: torch.Tensor | None = None
+
+    @property
+    def n_rows(self) -> int:
+        return int(self.tokens.numel())
+
+    @staticmethod
+    def pack(tokens, logp_train, logp_infer, cu_seqlens, adv, use, group_size: int, t_max: int,
+             temperature=1.0, device=None, row_index=None) -> "GRPOBatch":
+        """Build from per-row arrays and per-sample cu_seqlens (samples of one group contiguous)."""
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        cu = torch.as_tensor(cu_seqlens, dtype=torch.int64).cpu()
+        S = cu.numel() - 1
+        if S % group_size:
+            raise ValueError("sample count must be a multiple of the group size")
+        n_groups = S // group_size
+        lens = (cu[1:] - cu[:-1])
+        if lens.numel() and int(lens.max()) > t_max:
+            raise ValueError(f"t_max {t_max} below max token length {int(lens.max())}")
+        sample_of_row = torch.repeat_interleave(torch.arange(S, dtype=torch.int32), lens).to(dev)
+        temp = torch.as_tensor(temperature, dtype=torch.float64)
+        temp = (temp.expand(S) if temp.ndim == 0 else temp).contiguous().to(dev)
+        if bool((temp <= 0).any()):
+            raise ValueError("temperature must be > 0")
+        norm = torch.full((S,), 1.0 / (n_groups * group_size * t_max), dtype=torch.float64, device=dev)
+        f64 = lambda x: torch.as_tensor(x, dtype=torch.float64).to(dev).contiguous()
+        return GRPOBatch(
+            tokens=torch.as_tensor(tokens, dtype=torch.int32).to(dev).contiguous(),
+            logp_train=f64(logp_train), logp_infer=f64(logp_infer), sample_of_row=sample_of_row,
+            adv=f64(adv), use=torch.as_tensor(use, dtype=torch.uint8).to(dev).contiguous(), temperature=temp,
+            norm=norm, group_rows=cu[::group_size].to(dev).contiguous(), n_groups=n_groups,
+            group_size=group_size, t_max=t_max,
+            row_index=None if row_index is None else torch.as_tensor(row_index, dtype=torch.int64).to(dev))
+
+
+@dataclass
+class GRPOForward:
+    objective: torch.Tensor  # 0-d f64 (J, to maximise)
+    group_sums: torch.Tensor  # [n_groups] f64: sum of token terms per group
+    logp: torch.Tensor
+    lse: torch.Tensor
+    term: torch.Tensor
+    coef: torch.Tensor
+    flags: torch.Tensor
+
+
+def grpo_forward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = ClipConfig(), *, stream=None,
+                 group=None) -> GRPOForward:
+    """K4 over every row + fixed-order per-group sums; J = sum_g (S_g / (G T_max)) / n_groups.
+
+    `logits` is [rows, V] (row_stride = V) in bf16/f32/f64.  With a process group, rows are this
+    rank's share and the per-group sums are all-reduced (one f64 vector)."""
+    if logits.ndim != 2:
+        raise ValueError("logits must be [rows, vocab]")
+    logits = logits.contiguous()
+    R, V = batch.n_rows, logits.shape[1]
+    dev = logits.device
+    f64 = dict(dtype=torch.float64, device=dev)
+    logp, lse, term, coef = (torch.empty(R, **f64) for _ in range(4))
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    s = L.stream_handle(stream)
+    c = clip.c_struct()
+    L.call("rlk_grpo_fwd", L.ptr(logits), L.dtype_code(logits.dtype), R, V, V, L.ptr(batch.row_index),
+           L.ptr(batch.tokens), L.ptr(batch.logp_train), L.ptr(batch.logp_infer), L.ptr(batch.sample_of_row),
+           L.ptr(batch.adv), L.ptr(batch.use), L.ptr(batch.temperature), L.ptr(batch.norm), L.C.byref(c),
+           L.ptr(logp), L.ptr(lse), L.ptr(term), L.ptr(coef), L.ptr(flags), s)
+    gs = torch.empty(batch.n_groups, **f64)
+    L.call("rlk_segment_sum_f64", L.ptr(term), L.ptr(batch.group_rows), batch.n_groups, L.ptr(gs), s)
+    if group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(gs, group=group)
+    scaled = gs / float(batch.group_size * batch.t_max)
+    tot = torch.empty(1, **f64)
+    seg = torch.tensor([0, batch.n_groups], dtype=torch.int64, device=dev)
+    L.call("rlk_segment_sum_f64", L.ptr(scaled), L.ptr(seg), 1, L.ptr(tot), s)
+    return GRPOForward(tot[0] / batch.n_groups, gs, logp, lse, term, coef, flags)
+
+
+def grpo_backward(logits: torch.Tensor, batch: GRPOBatch, fwd: GRPOForward, grad_scale: torch.Tensor | float = 1.0,
+                  grad_dtype: torch.dtype | None = None, *, stream=None) -> torch.Tensor:
+    """K5: dJ/dlogits for one-row-per-token batches, scaled by `grad_scale` (the autograd grad_out)."""
+    R, V = logits.shape
+    coef = fwd.coef if (isinstance(grad_scale, float) and grad_scale == 1.0) else fwd.coef * grad_scale
+    coef = coef.contiguous()
+    temp_tok = batch.temperature[batch.sample_of_row.long()].contiguous()
+    grad = torch.empty((R, V), dtype=grad_dtype or logits.dtype, device=logits.device)
+    L.call("rlk_grpo_bwd", L.ptr(logits), L.dtype_code(logits.dtype), R, V, V, L.ptr(batch.row_index), None, None,
+           L.ptr(batch.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(coef), L.ptr(grad),
+           L.dtype_code(grad.dtype), V, L.stream_handle(stream))
+    return grad
+
+
+class GRPOTokenLoss(torch.autograd.Function):
+    """Autograd wrapper: forward returns J (maximised objective); backward runs K5."""
+
+    @staticmethod
+    def forward(ctx, logits, batch: GRPOBatch, clip: ClipConfig):
+        fwd = grpo_forward(logits, batch, clip)
+        ctx.save_for_backward(logits)
+        ctx.batch, ctx.fwd = batch, fwd
+        return fwd.objective
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        (logits,) = ctx.saved_tensors
+        g = grpo_backward(logits, ctx.batch, ctx.fwd, grad_out.to(torch.float64))
+        return g, None, None
+
+
+def grpo_token_objective(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = ClipConfig()) -> torch.Tensor:
+    return GRPOTokenLoss.apply(logits, batch, clip)
+
+
+def token_logprobs(logits2d: torch.Tensor, tokens: Sequence[int], temperature: float = 1.0,
+                   rows: Sequence[int] | None = None) -> torch.Tensor:
+    """log p(token) under z / T for the given rows (K4 with a log-prob-only epilogue)."""
+    n = len(tokens)
+    dev = logits2d.device
+    zeros = np.zeros(n)
+    b = GRPOBatch.pack(tokens, zeros, zeros, [0, n], [0.0], [1], 1, max(n, 1), temperature=[temperature],
+                       device=dev, row_index=rows)
+    return grpo_forward(logits2d, b).logp
+
+
+# ----------------------------------------------------------------------------- object API (reference)
+def _require_logps(sample: Sample) -> None:
+    if sample.train_logps is None:
+        raise ValueError(f"sample for prompt {sample.prompt_id} is missing train log-probs")
+    if len(sample.infer_logps) != len(sample.tokens):
+        raise ValueError("infer log-probs do not align with tokens")
+
+
+def _pack_masked_batch(batch: MaskedBatch, params: ParamTable) -> tuple[GRPOBatch, list]:
+    """USE samples' tokens -> packed rows reading logits row context_id * max_len + t."""
+    V, T = params.vocab_size, params.max_len
+    toks, lt, li, rows, cu, adv, temps = [], [], [], [], [0], [], []
+    group_rows = [0]
+    for mg in batch.groups:
+        for sample, a, mask in zip(mg.group.samples, mg.advantages, mg.masks):
+            if mask is not Mask.USE:
+                continue
+            _require_logps(sample)
+            tau = sample.gen_temperature
+            if tau != 1.0 and tau <= 0:
+                raise ValueError("temperature must be > 0")
+            if not 0 <= sample.context_id < params.context_count:
+                raise IndexError(f"context_id {sample.context_id} out of range [0, {params.context_count})")
+            for t, tok in enumerate(sample.tokens):
+                if not 0 <= t < T:
+                    raise IndexError(f"position {t} out of range [0, {T})")
+                tok = int(tok)
+                if not -V <= tok < V:
+                    raise IndexError(f"index {tok} is out of bounds for axis 0 with size {V}")
+                toks.append(tok % V)  # numpy indexing wraps negative ids (objective.py:244)
+                rows.append(sample.context_id * T + t)
+            lt.extend(float(x) for x in sample.train_logps)
+            li.extend(float(x) for x in sample.infer_logps)
+            cu.append(len(toks))
+            adv.append(float(a))
+            temps.append(float(tau))
+        group_rows.append(len(cu) - 1)
+    lt_a, li_a = np.asarray(lt, dtype=np.float64), np.asarray(li, dtype=np.float64)
+    if not (np.isfinite(lt_a).all() and np.isfinite(li_a).all()):
+        raise ValueError("log-probs must be finite")
+    S = len(adv)
+    dev = params.logits.device
+    cu_t = torch.tensor(cu, dtype=torch.int64)
+    lens = cu_t[1:] - cu_t[:-1]
+    G, n_groups = batch.groups[0].group.size, len(batch.groups)
+    b = GRPOBatch(
+        tokens=torch.tensor(toks, dtype=torch.int32, device=dev),
+        logp_train=torch.from_numpy(lt_a).to(dev), logp_infer=torch.from_numpy(li_a).to(dev),
+        sample_of_row=torch.repeat_interleave(torch.arange(S, dtype=torch.int32), lens).to(dev),
+        adv=torch.tensor(adv, dtype=torch.float64, device=dev),
+        use=torch.ones(S, dtype=torch.uint8, device=dev),
+        temperature=torch.tensor(temps, dtype=torch.float64, device=dev),
+        norm=torch.full((S,), 1.0 / (n_groups * G * batch.t_max), dtype=torch.float64, device=dev),
+        group_rows=torch.tensor([cu[g] for g in group_rows], dtype=torch.int64, device=dev),
+        n_groups=n_groups, group_size=G, t_max=batch.t_max,
+        row_index=torch.tensor(rows, dtype=torch.int64, device=dev))
+    return b, rows
+
+
+def objective_value(batch: MaskedBatch, params: ParamTable, clip: ClipConfig) -> float:
+    """Per group sum token terms / (G * T_max), averaged over groups (objective.py:230-250)."""
+    if not batch.groups:
+        return 0.0
+    b, _ = _pack_masked_batch(batch, params)
+    if b.n_rows == 0:
+        return 0.0
+    fwd = grpo_forward(params.logits.reshape(-1, params.vocab_size), b, clip)
+    if int(fwd.flags.item()) & 1:
+        raise ValueError("log-probs must be finite")
+    gs = fwd.group_sums.cpu().tolist()
+    G = batch.groups[0].group.size
+    total = 0.0
+    for g_sum in gs:
+        total += g_sum / (G * batch.t_max)
+    return total / len(batch.groups)
+
+
+def objective_gradient(batch: MaskedBatch, params: ParamTable, clip: ClipConfig) -> torch.Tensor:
+    """Exact gradient of objective_value w.r.t. the logit table (objective.py:253-283), f64, same shape.
+
+    Tokens that share a (context, position) row accumulate in the reference's order (K5, CSR rows)."""
+    grad = torch.zeros(params.shape, dtype=torch.float64, device=params.logits.device)
+    if not batch.groups:
+        return grad
+    b, rows = _pack_masked_batch(batch, params)
+    if b.n_rows == 0:
+        return grad
+    logits2d = params.logits.reshape(-1, params.vocab_size)
+    fwd = grpo_forward(logits2d, b, clip)
+    rows_np = np.asarray(rows, dtype=np.int64)
+    order = np.argsort(rows_np, kind="stable")
+    uniq, starts = np.unique(rows_np[order], return_index=True)
+    ptr = np.append(starts, len(order)).astype(np.int64)
+    dev = grad.device
+    temp_tok = b.temperature[b.sample_of_row.long()].contiguous()
+    g2d = grad.view(-1, params.vocab_size)
+    V = params.vocab_size
+    # keep every device argument referenced until the launch is enqueued (no freed temporaries)
+    urows = torch.from_numpy(uniq).to(dev)
+    row_ptr = torch.from_numpy(ptr).to(dev)
+    row_tok = torch.from_numpy(order.astype(np.int64)).to(dev)
+    L.call("rlk_grpo_bwd", L.ptr(logits2d), L.dtype_code(logits2d.dtype), len(uniq), V, V, L.ptr(urows),
+           L.ptr(row_ptr), L.ptr(row_tok), L.ptr(b.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(fwd.coef),
+           L.ptr(g2d), L.RLK_F64, V, L.stream_handle())
+    return grad
+
+
+def ascent_step(params: ParamTable, gradient, lr: float) -> ParamTable:
+    """New snapshot params + lr * gradient (objective.py:286-293), via rlk_scaled_add."""
+    if lr < 0:
+        raise ValueError("lr must be >= 0")
+    g = torch.as_tensor(np.asarray(gradient, dtype=np.float64)) if not isinstance(gradient, torch.Tensor) else gradient
+    if tuple(g.shape) != params.shape:
+        raise ValueError(f"gradient shape {tuple(g.shape)} != params shape {params.shape}")
+    p = params.logits.to(torch.float64).contiguous()
+    g = g.to(device=p.device, dtype=torch.float64).contiguous()
+    out = torch.empty_like(p)
+    L.call("rlk_scaled_add", L.ptr(p), L.ptr(g), float(lr), L.ptr(out), L.RLK_F64, p.numel(), L.stream_handle())
+    return ParamTable(out, copy=False)

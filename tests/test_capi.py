@@ -1,0 +1,45 @@
+"""The C-ABI library loads without a GPU and exports every entry point include/rlk.h declares."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    syms = set()
+    for h in (ROOT / "include").glob("*.h"):
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        syms |= set(re.findall(r"\b(rlk_[a-z0-9_]+)\s*\(", text))
+    return sorted(syms)
+
+
+def test_header_declares_hot_path():
+    syms = declared_symbols()
+    for s in ["rlk_fusion_sumsq", "rlk_fusion_finalize", "rlk_fusion_mask_bitmap", "rlk_fusion_merge",
+              "rlk_grpo_fwd", "rlk_grpo_bwd", "rlk_last_error"]:
+        assert s in syms
+
+
+def test_library_exports_all_declared_symbols():
+    from paper_2509_18883_b200 import _lib
+    if not _lib.LIB_PATH.exists():
+        from paper_2509_18883_b200._build import build
+        build()
+    handle = ctypes.CDLL(str(_lib.LIB_PATH))
+    missing = [s for s in declared_symbols() if not hasattr(handle, s)]
+    assert not missing, missing
+    assert handle.rlk_abi_version() == 1
+    # every declared symbol has a ctypes signature in the binding
+    assert not [s for s in declared_symbols() if s not in _lib.SIGNATURES]
+
+
+def test_invalid_arguments_map_to_value_error():
+    from paper_2509_18883_b200 import _lib as L
+    L.lib()
+    with pytest.raises(ValueError, match="expert count"):
+        L.call("rlk_fusion_sumsq", ctypes.byref(L.FusionPlanC(0, 0, 0, 1)), 9, 0, 0, 8, None)
+    with pytest.raises(ValueError, match="bad dtype"):
+        L.call("rlk_nonfinite_count", 8, 7, 1, 8, None)

@@ -1,0 +1,248 @@
+"""GPU parity: the sm_100a fusion kernels vs the reference's golden vectors and the CPU oracle."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fusion as OF
+from oracle import rng as OR
+from tests.helpers import bf16_bits_to_f64, bf16_round, mlp_dict_shapes, rne_bf16_bits, synth_state_dicts
+
+pytestmark = pytest.mark.gpu
+
+CFGS = {
+    "default": dict(),
+    "p05_s42": dict(dropout_p=0.5, seed=42),
+    "p05_s42_sq": dict(dropout_p=0.5, seed=42, erase_weighting="squared"),
+    "p03_s7_t1_w": dict(dropout_p=0.3, seed=7, target_norm=1.0, merge_weights=(0.5, 0.3, 0.2)),
+    "none_noerase": dict(target_norm=None, erase_mode=False),
+    "p09_s3_none": dict(dropout_p=0.9, seed=3, target_norm=None),
+}
+
+
+def _pt(x, dtype, dev):
+    from paper_2509_18883_b200.toy_env import ParamTable
+    return ParamTable(torch.from_numpy(np.asarray(x, dtype=np.float64).reshape(1, 1, -1)).to(dev, dtype))
+
+
+def _fuse(base, experts, cfgkw, dtype, dev, out_dtype=None):
+    from paper_2509_18883_b200 import fusion as F
+    b = _pt(base, dtype, dev)
+    taus = [F.task_vector(_pt(e, dtype, dev), b) for e in experts]
+    return F.fuse(b, taus, F.FusionConfig(**cfgkw), out_dtype=out_dtype)
+
+
+@pytest.mark.parametrize("cname", list(CFGS))
+def test_fuse_kat_f64(cuda, golden_fusion, cname):
+    base = golden_fusion["kat/base"]
+    experts = [golden_fusion[f"kat/expert{k}"] for k in range(3)]
+    fused, st = _fuse(base, experts, CFGS[cname], torch.float64, cuda)
+    ref = golden_fusion[f"kat/{cname}/fused"]
+    got = fused.numpy().ravel()
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-15)
+    assert list(st.erased_counts) == list(golden_fusion[f"kat/{cname}/erased"])
+    assert list(st.dropout_kept_fraction) == list(golden_fusion[f"kat/{cname}/kept"])
+    np.testing.assert_allclose(st.norms_before, golden_fusion[f"kat/{cname}/norms_before"], rtol=1e-13)
+    np.testing.assert_allclose(st.norms_after_normalize, golden_fusion[f"kat/{cname}/norms_after"], rtol=1e-13)
+    # erase decisions bit-exact: zero pattern of the fused-minus-base contribution
+    assert (got == base).sum() == (ref == base).sum()
+
+
+@pytest.mark.parametrize("fast", ["1", "0"])
+@pytest.mark.parametrize("cname", ["default", "p05_s42", "p05_s42_sq", "p03_s7_t1_w", "p09_s3_none"])
+def test_fuse_bf16_exact(cuda, golden_fusion, cname, fast, monkeypatch):
+    """bf16 in / bf16 out must equal RNE_bf16(reference f64 output) bit for bit."""
+    monkeypatch.setenv("RLK_MERGE_FAST", fast)
+    base = golden_fusion["bf16/base"]
+    experts = [golden_fusion[f"bf16/expert{k}"] for k in range(3)]
+    fused, st = _fuse(base, experts, CFGS[cname], torch.bfloat16, cuda)
+    got = fused.logits.reshape(-1).view(torch.int16).cpu().numpy().view(np.uint16)
+    ref = rne_bf16_bits(golden_fusion[f"bf16/{cname}/fused"])
+    mism = np.flatnonzero(got != ref)
+    assert mism.size == 0, (mism[:10], got[mism[:10]], ref[mism[:10]])
+    assert list(st.erased_counts) == list(golden_fusion[f"bf16/{cname}/erased"])
+    assert list(st.dropout_kept_fraction) == list(golden_fusion[f"bf16/{cname}/kept"])
+    # f64 output from bf16 inputs: same numbers as the f64 reference
+    fused64, _ = _fuse(base, experts, CFGS[cname], torch.bfloat16, cuda, out_dtype=torch.float64)
+    np.testing.assert_allclose(fused64.numpy().ravel(), golden_fusion[f"bf16/{cname}/fused"], rtol=1e-12,
+                               atol=1e-16)
+
+
+def test_staged_functions(cuda, golden_fusion):
+    from paper_2509_18883_b200 import core, fusion as F
+    base = golden_fusion["kat/base"]
+    experts = [golden_fusion[f"kat/expert{k}"] for k in range(3)]
+    b = _pt(base, torch.float64, cuda)
+    taus = [F.task_vector(_pt(e, torch.float64, cuda), b) for e in experts]
+    nm = F.normalize_magnitudes(taus, F.FusionConfig())
+    for k in range(3):
+        np.testing.assert_allclose(nm[k].delta.cpu().numpy().ravel(), golden_fusion[f"stage/normalized{k}"],
+                                   rtol=1e-12, atol=1e-17)
+    r = core.make_rng(11, "stage")
+    dp = F.dropout_prune(taus[0], 0.4, r)
+    got = dp.delta.cpu().numpy().ravel()
+    ref = golden_fusion["stage/dropout0"]
+    np.testing.assert_array_equal(got == 0, ref == 0)  # bit-exact mask
+    np.testing.assert_array_equal(got, ref)  # (d / 0.6 exact division)
+    assert r.next_u64() == int(golden_fusion["stage/dropout_rng_after"][0])  # rng advanced like the loop
+    for w in ("sum", "squared"):
+        er = F.erase_minority(taus, w)
+        for k in range(3):
+            np.testing.assert_array_equal(er[k].delta.cpu().numpy().ravel(), golden_fusion[f"stage/erase_{w}{k}"])
+    tv = [F.TaskVector(np.array([[[v]]])) for v in (0.3, 0.1, -0.2)]
+    assert [float(t.delta.item()) for t in F.erase_minority(tv)] == [0.3, 0.1, 0.0]
+
+
+def test_fuse_validation_messages(cuda):
+    from paper_2509_18883_b200 import fusion as F
+    b = _pt(np.zeros(8), torch.float64, cuda)
+    e = _pt(np.ones(8), torch.float64, cuda)
+    with pytest.raises(ValueError, match="need at least one task vector"):
+        F.fuse(b, [], F.FusionConfig())
+    with pytest.raises(ValueError, match="merge_weights length"):
+        F.fuse(b, [F.task_vector(e, b)], F.FusionConfig(merge_weights=(0.5, 0.5)))
+    with pytest.raises(ValueError, match="cannot take mean norm of all-zero task vectors"):
+        F.fuse(b, [F.task_vector(b, b)], F.FusionConfig())
+    with pytest.raises(ValueError, match="logits must be finite"):
+        F.ParamTable(torch.tensor([[[1.0, float("nan")]]], device=cuda))
+    # identity round trip: 1 expert, w=1, p=0, erase off
+    fused, _ = F.fuse(b, [F.task_vector(e, b)], F.FusionConfig(target_norm=None, erase_mode=False))
+    assert torch.equal(fused.logits, e.logits)
+    # opposite deltas cancel back to the base
+    e2 = _pt(-np.ones(8), torch.float64, cuda)
+    fused, st = F.fuse(b, [F.task_vector(e, b), F.task_vector(e2, b)], F.FusionConfig())
+    assert torch.equal(fused.logits, b.logits)
+
+
+def _oracle_dict(base, experts, cfgkw):
+    out, stats = {}, {}
+    for name in base:
+        f, s = OF.fuse(base[name], [e[name] for e in experts], **cfgkw)
+        out[name], stats[name] = f, s
+    return out, stats
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("cfgkw", [dict(), dict(dropout_p=0.5, seed=42), dict(dropout_p=0.3, seed=0,
+                                                                             erase_weighting="squared")])
+def test_state_dict_vs_oracle(cuda, dtype, cfgkw):
+    """Config-1 shaped MLP dict (scaled 1/4): every tensor equals the per-tensor reference fuse."""
+    from paper_2509_18883_b200 import fusion as F
+    rnd = bf16_round if dtype == torch.bfloat16 else (lambda x: np.asarray(x, np.float32).astype(np.float64))
+    base, experts = synth_state_dicts(mlp_dict_shapes(4), 3, seed=1, dtype_round=rnd)
+    to = lambda d: {k: torch.from_numpy(v).to(cuda, dtype) for k, v in d.items()}
+    outs, rep = F.fuse_state_dict(to(base), [to(e) for e in experts], F.FusionConfig(**cfgkw))
+    ref, rstats = _oracle_dict(base, experts, cfgkw)
+    for name in base:
+        got = outs[name].reshape(-1)
+        if dtype == torch.bfloat16:
+            g = got.view(torch.int16).cpu().numpy().view(np.uint16)
+            r = rne_bf16_bits(ref[name])
+            assert (g != r).sum() == 0, name
+        else:
+            np.testing.assert_array_equal(got.cpu().numpy(), ref[name].astype(np.float32), err_msg=name)
+        st = rep.stats(name)
+        assert list(st.erased_counts) == rstats[name]["erased"], name
+        assert list(st.dropout_kept_fraction) == rstats[name]["kept"], name
+        np.testing.assert_allclose(st.norms_before, rstats[name]["norms_before"], rtol=1e-13)
+
+
+def test_dropout_bitmap_equals_inline(cuda):
+    from paper_2509_18883_b200 import fusion as F
+    base, experts = synth_state_dicts(mlp_dict_shapes(4), 3, seed=2, dtype_round=bf16_round)
+    to = lambda d: {k: torch.from_numpy(v).to(cuda, torch.bfloat16) for k, v in d.items()}
+    cfg = F.FusionConfig(dropout_p=0.5, seed=9)
+    res = []
+    for mode in ("1", "2"):
+        os.environ["RLK_DROPOUT_MODE"] = mode
+        try:
+            outs, rep = F.fuse_state_dict(to(base), [to(e) for e in experts], cfg)
+        finally:
+            del os.environ["RLK_DROPOUT_MODE"]
+        assert rep.call.dropout_mode == int(mode)
+        res.append((outs, rep.call.counters.cpu()))
+    for k in res[0][0]:
+        assert torch.equal(res[0][0][k], res[1][0][k])
+    assert torch.equal(res[0][1], res[1][1])
+
+
+def test_mask_bitmap_bit_exact(cuda):
+    """K2 keep bits == the reference's `uniform >= p` draws, incl. a far index window."""
+    from paper_2509_18883_b200 import _lib as L
+    from paper_2509_18883_b200.core import fusion_child_seeds, keep_threshold
+    for p in (0.3, 0.5, 0.9):
+        seeds = fusion_child_seeds(42, 3)
+        n_bits = 1 << 20
+        wpr = n_bits // 32
+        bm = torch.empty(3 * wpr, dtype=torch.int32, device=cuda)
+        L.call("rlk_fusion_mask_bitmap", (L.C.c_uint64 * 3)(*seeds), 3, keep_threshold(p), n_bits, L.ptr(bm), wpr,
+               L.stream_handle())
+        bits = np.unpackbits(bm.cpu().numpy().view(np.uint8), bitorder="little").reshape(3, n_bits)
+        for i in range(3):
+            ref = OR.keep_mask(OR.fusion_child_seed(42, i), 0, n_bits, p)
+            assert np.array_equal(bits[i].astype(bool), ref)
+
+
+def test_fast_path_equals_exact_path_random(cuda, monkeypatch):
+    """f32 fast path with certified guards == pure reference-order f64 path, on 24M bf16 elements
+    including crafted near-ties and midpoint cases."""
+    from paper_2509_18883_b200 import fusion as F
+    g = torch.Generator(device=cuda).manual_seed(0)
+    n = 24 * 1024 * 1024 + 7
+    base = (torch.randn(n, device=cuda, generator=g) * 0.02).to(torch.bfloat16)
+    experts = [(base.float() + torch.randn(n, device=cuda, generator=g) * 1e-3 * (i + 1)).to(torch.bfloat16)
+               for i in range(3)]
+    # near-ties: expert 2 = base - (d0 + d1) rounded
+    idx = torch.arange(0, n, 97, device=cuda)
+    d0 = experts[0].float()[idx] - base.float()[idx]
+    d1 = experts[1].float()[idx] - base.float()[idx]
+    experts[2][idx] = (base.float()[idx] - d0 - d1).to(torch.bfloat16)
+    for cfg in (F.FusionConfig(), F.FusionConfig(dropout_p=0.5, seed=1), F.FusionConfig(erase_weighting="squared"),
+                F.FusionConfig(target_norm=None)):
+        outs = []
+        for fast in ("1", "0"):
+            monkeypatch.setenv("RLK_MERGE_FAST", fast)
+            o, rep = F.fuse_state_dict({"w": base}, [{"w": e} for e in experts], cfg)
+            outs.append((o["w"], rep.call.counters.clone()))
+        assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16)), cfg
+        assert torch.equal(outs[0][1], outs[1][1]), cfg
+
+
+def test_sharded_items_identical(cuda):
+    """Pieces split over 2/4 'ranks' (item-aligned) give bit-identical norms, outputs and counters."""
+    from paper_2509_18883_b200 import fusion as F
+    base, experts = synth_state_dicts({"a": (3000, 517), "b": (70001,), "c": (1024, 1024)}, 3, seed=3,
+                                      dtype_round=bf16_round)
+    names = list(base)
+    to = lambda a: torch.from_numpy(a.reshape(-1)).to(cuda, torch.bfloat16)
+    B = [to(base[k]) for k in names]
+    E = [[to(e[k]) for k in names] for e in experts]
+    layout = F.FusionLayout([b.numel() for b in B])
+    cfg = F.FusionConfig(dropout_p=0.5, seed=5)
+    w = (1 / 3, 1 / 3, 1 / 3)
+    results = []
+    for world in (1, 2, 4):
+        outs = [torch.empty_like(b) for b in B]
+        partials = torch.zeros(layout.n_items * 3, dtype=torch.float64, device=cuda)
+        calls = []
+        for rank in range(world):
+            pieces = [F.Piece(t, lo, B[t][lo:hi], [E[i][t][lo:hi] for i in range(3)], outs[t][lo:hi])
+                      for t, lo, hi in layout.partition(world, rank)]
+            c = F.FusionCall(pieces, layout, 3, cfg)
+            c.partials = partials
+            from paper_2509_18883_b200 import _lib as L
+            L.call("rlk_fusion_sumsq", L.C.byref(c.plan.c), 3, L.RLK_BF16, 0, L.ptr(partials), L.stream_handle())
+            calls.append(c)
+        counters = torch.zeros((3, 6), dtype=torch.int64, device=cuda)
+        for c in calls:
+            L.call("rlk_fusion_finalize", L.ptr(partials), L.ptr(layout.tensor_items_device(cuda)), 3, 3, 1, 0.0,
+                   L.ptr(c.sumsq), L.ptr(c.scale), L.ptr(c.status), L.stream_handle())
+            c.merge(w)
+            counters += c.counters
+        results.append((calls[0].sumsq.clone(), [o.clone() for o in outs], counters))
+    for r in results[1:]:
+        assert torch.equal(r[0], results[0][0])
+        for a, b in zip(r[1], results[0][1]):
+            assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+        assert torch.equal(r[2], results[0][2])

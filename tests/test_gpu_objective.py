@@ -1,0 +1,169 @@
+"""GPU parity: the GRPO kernels (K4/K5) vs the reference's golden vectors and the CPU oracle."""
+import json
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import objective as OO
+from tests.helpers import bf16_round
+
+pytestmark = pytest.mark.gpu
+
+
+def _rebuild_batch(g, cname):
+    from paper_2509_18883_b200 import core, objective as O
+    meta = json.loads(str(g[f"{cname}/meta"]))
+    G = meta["G"]
+    groups = []
+    for gi in range(meta["n_groups"]):
+        samples = []
+        for s in meta["samples"][gi * G:(gi + 1) * G]:
+            rw = core.RewardOutcome(core.RewardKind(s["kind"]), s["reward"])
+            samples.append(core.Sample(prompt_id=gi, context_id=s["ctx"], version_id=0, tokens=tuple(s["tokens"]),
+                                       infer_logps=tuple(s["li"]), status=core.SampleStatus.COMPLETE, t_start=0,
+                                       train_logps=tuple(s["lt"]), reward=rw, gen_temperature=s["tau"]))
+        groups.append(core.Group(gi, tuple(samples)))
+    batch = O.apply_masks(groups, meta["t_max"])
+    for mg, gi in zip(batch.groups, range(meta["n_groups"])):
+        for a, m, s in zip(mg.advantages, mg.masks, meta["samples"][gi * G:(gi + 1) * G]):
+            assert a == s["adv"] and m.value == s["mask"]
+    return batch, O.ClipConfig(guard_positive=meta["guard"])
+
+
+@pytest.mark.parametrize("cname", ["small", "mid", "mid_literal"])
+def test_objective_kat(cuda, golden_objective, cname):
+    from paper_2509_18883_b200 import objective as O
+    from paper_2509_18883_b200.toy_env import ParamTable
+    batch, clip = _rebuild_batch(golden_objective, cname)
+    params = ParamTable(golden_objective[f"{cname}/logits"])
+    J = O.objective_value(batch, params, clip)
+    assert J == pytest.approx(float(golden_objective[f"{cname}/value"][0]), rel=1e-12, abs=1e-16)
+    grad = O.objective_gradient(batch, params, clip).cpu().numpy()
+    np.testing.assert_allclose(grad, golden_objective[f"{cname}/grad"], rtol=1e-10, atol=1e-16)
+    # ascent_step
+    p2 = O.ascent_step(params, grad, 0.5)
+    np.testing.assert_array_equal(p2.numpy(), params.numpy() + 0.5 * grad)
+
+
+def _synthetic_rows(R_per_sample, S, V, G, seed=0, tau=1.0, masked=()):
+    """SURVEY 8(d) config-5 style rows: logits N(0, 2^2) + a peaked column, tokens ~ softmax."""
+    g = np.random.default_rng(seed)
+    R = R_per_sample * S
+    logits = g.normal(0, 2.0, (R, V)).astype(np.float32)
+    peak = g.integers(0, V, R)
+    logits[np.arange(R), peak] += 8.0
+    logits = bf16_round(logits)
+    toks = np.empty(R, dtype=np.int64)
+    lt = np.empty(R)
+    for r in range(R):
+        lp = OO.log_token_dist(logits[r], tau)
+        p = np.exp(lp)
+        toks[r] = g.choice(V, p=p / p.sum())
+        lt[r] = lp[toks[r]] + g.normal(0, 0.3)
+    li = lt + g.normal(0, 0.05, R)
+    rewards = g.integers(0, 2, S).astype(float)
+    adv = np.zeros(S)
+    for k in range(S // G):
+        r = rewards[k * G:(k + 1) * G]
+        adv[k * G:(k + 1) * G] = (r - r.mean()) / max(r.std(), 1e-8)
+    use = np.ones(S, dtype=np.uint8)
+    for m in masked:
+        use[m] = 0
+    cu = np.arange(S + 1) * R_per_sample
+    return logits, toks, lt, li, adv, use, cu
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("tau", [1.0, 0.7])
+def test_tensor_api_vs_oracle(cuda, dtype, tau):
+    from paper_2509_18883_b200 import objective as O
+    V, G, S, Rps, T_max = 131072, 4, 8, 12, 16
+    logits, toks, lt, li, adv, use, cu = _synthetic_rows(Rps, S, V, G, seed=1, tau=tau, masked=(3,))
+    b = O.GRPOBatch.pack(toks, lt, li, cu, adv, use, G, T_max, temperature=tau, device=cuda)
+    lg = torch.from_numpy(logits).to(cuda, dtype)
+    fwd = O.grpo_forward(lg, b)
+    clip = dict(eps_neg_low=0.2, eps_pos_high=0.2, eps_neg_high=3.0, tis_cap=2.0, guard_positive=True)
+    sor = np.repeat(np.arange(S), Rps)
+    norm = 1.0 / ((S // G) * G * T_max)
+    logp, term, coef = OO.token_terms(logits, None, toks, lt, li, sor, adv, use, [tau] * S, clip, norm=norm)
+    J = OO.objective(term, list(cu[::G]), G, T_max)
+    got_logp = fwd.logp.cpu().numpy()
+    act = use[sor].astype(bool)
+    np.testing.assert_allclose(got_logp[act], logp[act], rtol=0, atol=2e-5)
+    np.testing.assert_allclose(fwd.term.cpu().numpy(), term, rtol=1e-4, atol=1e-6)
+    assert float(fwd.objective) == pytest.approx(J, rel=1e-3)  # north-star tolerance
+    assert int(fwd.flags.item()) == 0
+    # masked sample rows contribute nothing and are not read
+    assert np.all(fwd.coef.cpu().numpy()[~act] == 0)
+    # backward vs oracle gradient rows
+    grad = O.grpo_backward(lg, b, fwd, grad_dtype=torch.float32).cpu().numpy()
+    ref = OO.gradient_rows(logits, None, toks, coef, [tau] * len(toks), logits.shape)
+    scale = np.abs(coef).max()
+    np.testing.assert_allclose(grad, ref, rtol=0, atol=2e-4 * scale)
+
+
+def test_autograd_and_bf16_grad(cuda):
+    from paper_2509_18883_b200 import objective as O
+    V, G, S, Rps, T_max = 4096, 2, 4, 6, 8
+    logits, toks, lt, li, adv, use, cu = _synthetic_rows(Rps, S, V, G, seed=2)
+    b = O.GRPOBatch.pack(toks, lt, li, cu, adv, use, G, T_max, device=cuda)
+    lg = torch.from_numpy(logits).to(cuda, torch.bfloat16).requires_grad_(True)
+    J = O.grpo_token_objective(lg, b)
+    (-2.0 * J).backward()
+    fwd = O.grpo_forward(lg.detach(), b)
+    ref = O.grpo_backward(lg.detach(), b, fwd, grad_dtype=torch.float32) * -2.0
+    np.testing.assert_allclose(lg.grad.float().cpu().numpy(), ref.cpu().numpy(), rtol=1e-2, atol=1e-9)
+
+
+def test_f64_finite_difference(cuda):
+    """objective_gradient matches central finite differences of objective_value."""
+    from paper_2509_18883_b200 import core, objective as O
+    from paper_2509_18883_b200.toy_env import ParamTable
+    g = np.random.default_rng(4)
+    C, T, V, G = 1, 4, 6, 3
+    logits = g.normal(0, 1.0, (C, T, V))
+    samples = []
+    for si in range(G):
+        toks = tuple(int(x) for x in g.integers(0, V, T))
+        lt = tuple(float(g.normal(-1.5, 0.3)) for _ in toks)
+        li = tuple(x + float(g.normal(0, 0.05)) for x in lt)
+        rw = core.RewardOutcome.passed() if si % 2 else core.RewardOutcome.failed()
+        samples.append(core.Sample(0, 0, 0, toks, li, core.SampleStatus.COMPLETE, 0, train_logps=lt, reward=rw,
+                                   gen_temperature=0.8))
+    batch = O.apply_masks([core.Group(0, tuple(samples))], T)
+    clip = O.ClipConfig()
+    grad = O.objective_gradient(batch, ParamTable(logits), clip).cpu().numpy()
+    h = 1e-6
+    for idx in [(0, 0, 1), (0, 1, 3), (0, 3, 5), (0, 2, 0)]:
+        lp, lm = logits.copy(), logits.copy()
+        lp[idx] += h
+        lm[idx] -= h
+        fd = (O.objective_value(batch, ParamTable(lp), clip) - O.objective_value(batch, ParamTable(lm), clip)) / (2 * h)
+        assert fd == pytest.approx(grad[idx], rel=1e-5, abs=1e-9)
+
+
+def test_log_token_dist_and_trace(cuda):
+    from paper_2509_18883_b200 import core
+    from paper_2509_18883_b200.toy_env import ParamTable, TrainEngine, log_token_dist, logprob_trace
+    g = np.random.default_rng(6)
+    logits = g.normal(0, 1.5, (2, 3, 50))
+    pt = ParamTable(logits)
+    for tau in (1.0, 0.6):
+        got = log_token_dist(pt, TrainEngine(), 1, 2, tau).cpu().numpy()
+        np.testing.assert_allclose(got, OO.log_token_dist(logits[1, 2], tau), rtol=1e-13, atol=1e-14)
+    s = core.Sample(0, 1, 0, (3, 7, 9), (0.0, 0.0, 0.0), core.SampleStatus.COMPLETE, 0, gen_temperature=0.9)
+    tr = logprob_trace(pt, TrainEngine(), s)
+    ref = [OO.log_token_dist(logits[1, t], 0.9)[tok] for t, tok in enumerate(s.tokens)]
+    np.testing.assert_allclose(tr, ref, rtol=1e-13)
+    with pytest.raises(IndexError):
+        log_token_dist(pt, TrainEngine(), 2, 0)
+
+
+def test_bad_token_flag(cuda):
+    from paper_2509_18883_b200 import objective as O
+    V = 256
+    b = O.GRPOBatch.pack([5, V + 3], [-1.0, -1.0], [-1.0, -1.0], [0, 1, 2], [1.0, -1.0], [1, 1], 2, 4, device=cuda)
+    fwd = O.grpo_forward(torch.zeros((2, V), device=cuda, dtype=torch.bfloat16), b)
+    assert int(fwd.flags.item()) & 2
