@@ -151,6 +151,11 @@ int rlk_nonfinite_count(const void* x, int dtype, uint64_t n, unsigned long long
 int rlk_scaled_add(const void* a, const void* b, double alpha, void* out, int dtype, uint64_t n,
                    void* stream);
 
+/* Benchmark / test data: out[i] = RN(base[i] + std * N(0,1)) with a counter-hash normal keyed by
+ * (seed, j0 + i); base may be NULL (then 0) and has out's dtype. */
+int rlk_synth_normal(void* out, int dtype, uint64_t n, uint64_t j0, uint64_t seed, double std_dev,
+                     const void* base, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,7 @@ SIGNATURES = {
     "rlk_logsoftmax_rows": (_I, [_P, _I, _U64, _U64, _U64, _P, _P, _P, _I, _P]),
     "rlk_nonfinite_count": (_I, [_P, _I, _U64, _P, _P]),
     "rlk_scaled_add": (_I, [_P, _P, _D, _P, _I, _U64, _P]),
+    "rlk_synth_normal": (_I, [_P, _I, _U64, _U64, _U64, _D, _P, _P]),
     "rlk_loader_create": (_P, [_U64, _I]),
     "rlk_loader_destroy": (None, [_P]),
     "rlk_loader_stage": (_I, [_P, _P, _P, _U64, _P]),

@@ -102,3 +102,40 @@ int rlk_scaled_add(const void* a, const void* b, double alpha, void* out, int dt
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// Synthetic parameters for benchmarks / tests: out[i] = RN_dtype(base[i] + std * N(0,1)), where the
+// normal deviate is a Box-Muller transform of mix64(seed ^ mix64(j0 + i)).  Counter-based, so a slice
+// [j0, j0 + n) has the same values at any world size / piece split.
+namespace rlk {
+template <int DT, int BT>
+__global__ void k_synth(void* __restrict__ out, uint64_t n, uint64_t j0, uint64_t seed, double stdv,
+                        const void* __restrict__ base) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t h = mix64(seed ^ mix64(j0 + i + 1));
+    const float u1 = ((uint32_t)(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
+    const float u2 = (uint32_t)(h & 0xffffffu) * (1.0f / 16777216.0f);
+    const float z = sqrtf(-2.0f * __logf(u1)) * __cosf(6.283185307f * u2);
+    const double b = base ? load_f64<BT>(base, i) : 0.0;
+    store_from_f64<DT>(out, i, b + stdv * (double)z);
+  }
+}
+}  // namespace rlk
+
+extern "C" int rlk_synth_normal(void* out, int dtype, uint64_t n, uint64_t j0, uint64_t seed, double stdv,
+                                const void* base, void* stream) {
+  if (n == 0) return RLK_OK;
+  RLK_REQUIRE(out != nullptr, "rlk_synth_normal: out is NULL");
+  RLK_REQUIRE(dtype >= 0 && dtype <= 2, "rlk_synth_normal: bad dtype %d", dtype);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t blocks = (n + 255) / 256;
+  const int grid = (int)(blocks < (uint64_t)sm_count() * 8 ? blocks : (uint64_t)sm_count() * 8);
+  // base (if any) has the same dtype as out
+  switch (dtype) {
+    case RLK_BF16: k_synth<RLK_BF16, RLK_BF16><<<grid, 256, 0, s>>>(out, n, j0, seed, stdv, base); break;
+    case RLK_F32: k_synth<RLK_F32, RLK_F32><<<grid, 256, 0, s>>>(out, n, j0, seed, stdv, base); break;
+    default: k_synth<RLK_F64, RLK_F64><<<grid, 256, 0, s>>>(out, n, j0, seed, stdv, base); break;
+  }
+  return launch_status("rlk_synth_normal");
+}

@@ -394,8 +394,52 @@ __device__ __forceinline__ uint32_t keep_bits_for(const MergeArgs& a, const uint
   return m;
 }
 
-template <int DTI, int DTO, int N>
-__global__ void __launch_bounds__(kThreads, 1) k_merge(MergeArgs a) {
+// Out-of-line exact evaluation used by the fast path for the rare elements whose guard tripped
+// (one copy of the f64 code instead of one per unrolled element).
+template <int N>
+struct FArr { float v[N]; };
+
+template <int N>
+__device__ __noinline__ double merge_elem_slow(float b, FArr<N> x, uint32_t keep, const MergeArgs* a,
+                                              const double* scale, uint32_t* nz, uint32_t* er) {
+  ElemConsts c;
+  double X[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    c.scale[i] = scale[i];
+    X[i] = (double)x.v[i];
+  }
+  return merge_elem_f64<N>((double)b, X, keep, *a, c, *nz, *er);
+}
+
+// Fast-path erase decisions of one element, recomputed with exactly the phase-1 arithmetic (scalar
+// IEEE ops give the same bits as the packed f32x2 ones); used to replace the counts of slow elements.
+template <int N>
+__device__ __forceinline__ uint32_t fast_opp_bits(float b, const float* x, uint32_t keep, const float* sr32,
+                                                  int erase_mode, bool delta) {
+  float k[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const float d = delta ? x[i] : fmaf(b, -1.f, x[i]);
+    k[i] = __fmul_rn(d, ((keep >> i) & 1u) ? sr32[i] : 0.f);
+  }
+  float v = erase_mode == 1 ? k[0] : __fmul_rn(k[0], fabsf(k[0]));
+#pragma unroll
+  for (int i = 1; i < N; ++i) v = __fadd_rn(v, erase_mode == 1 ? k[i] : __fmul_rn(k[i], fabsf(k[i])));
+  const float sg = copysignf(1.f, v);
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) m |= (uint32_t)(__fmul_rn(k[i], sg) < 0.f) << i;
+  return m;
+}
+
+__device__ __forceinline__ uint32_t word_of(const uint4& q, int p) {
+  return p == 0 ? q.x : (p == 1 ? q.y : (p == 2 ? q.z : q.w));
+}
+
+// FAST: bf16 -> bf16 with the f32x2 fast path; otherwise the reference-order f64 path only.
+template <int DTI, int DTO, int N, bool FAST>
+__global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ MergeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DTI>::size;
   constexpr int VEC = 16 / ESZ;
@@ -414,13 +458,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(MergeArgs a) {
   uint32_t q = 0;
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
     const ItemGeom g = item_geom(a.plan, item);
+    const double* scale = a.scale + (uint64_t)g.tensor * N;
     ElemConsts c;
-    float sr32[N], w32[N];
+    float sr32[N];
+    float wmax = 0.f;
+    bool fast_ok = FAST;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      c.scale[i] = __ldg(a.scale + (uint64_t)g.tensor * N + i);
+      c.scale[i] = __ldg(scale + i);
       sr32[i] = (float)(a.dropout_mode ? c.scale[i] / a.keep_prob : c.scale[i]);
-      w32[i] = (float)a.w[i];
+      wmax = fmaxf(wmax, (float)a.w[i]);
+      // k = d * sr cannot underflow for bf16 deltas (|d| >= 2^-133) when sr >= 2^-16
+      fast_ok = fast_ok && sr32[i] >= 0x1p-16f && sr32[i] < 0x1p100f;
     }
     uint32_t cnt_nz[N], cnt_er[N];
 #pragma unroll
@@ -435,134 +484,157 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(MergeArgs a) {
       const uint8_t* bm = sb + (N + 1) * SB;
       const uint32_t nvec = main_elems / VEC;
       const uint64_t out_base = g.start + off;
-      for (uint32_t v = tid; v < nvec; v += kCThreads) {
-        const uint32_t le = v * VEC;
-        if constexpr (DTI == RLK_BF16 && DTO == RLK_BF16) {
-          if (a.fast) {
-            // ---- f32 fast path with certified guards; falls back to merge_elem_f64 per element.
-            float b[8], x[N][8];
-            if (wb) VecIO<RLK_BF16>::f32(lds128(sb + v * 16), b);
-            else {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) b[e] = 0.f;
-            }
-#pragma unroll
-            for (int i = 0; i < N; ++i) VecIO<RLK_BF16>::f32(lds128(sb + (i + (wb ? 1 : 0)) * SB + v * 16), x[i]);
+      if (FAST && fast_ok) {
+        if constexpr (FAST) {
+          // ---------------- phase 1: branch-free, two elements per f32x2 op
+          const float2 neg1 = make_float2(-1.f, -1.f);
+          const float cv = a.erase_mode == 1 ? 0x1p-20f : 0x1p-19f;
+          for (uint32_t v = tid; v < nvec; v += kCThreads) {
+            const uint32_t le = v * 8;
+            const uint4 bw4 = wb ? lds128(sb + v * 16) : make_uint4(0, 0, 0, 0);
+            uint4 xw4[N];
             uint32_t kb[N];
 #pragma unroll
             for (int i = 0; i < N; ++i) {
+              xw4[i] = lds128(sb + (i + (wb ? 1 : 0)) * SB + v * 16);
               if (a.dropout_mode == 2) kb[i] = bm[i * BMB + (le >> 3)];
               else if (a.dropout_mode == 1) {
                 kb[i] = 0;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) kb[i] |= (uint32_t)keep_draw(a.seed[i], jtensor0 + off + le + e, a.thresh) << e;
+                for (int e = 0; e < 8; ++e)
+                  kb[i] |= (uint32_t)keep_draw(a.seed[i], jtensor0 + off + le + e, a.thresh) << e;
               } else kb[i] = 0xffu;
             }
-            float y[8];
-            uint32_t slowmask = 0, slowbits[8];
+            uint32_t outw[4];
+            uint32_t slowm = 0;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              float d[N], k[N];
-              uint32_t nzm = 0, erm = 0;
+            for (int p = 0; p < 4; ++p) {
+              const uint32_t bw = word_of(bw4, p);
+              const float2 b2 = make_float2(bf16_lo(bw), bf16_hi(bw));
+              float2 k2[N];
+              float2 aa = make_float2(0.f, 0.f);
+              bool nzl = false, nzh = false;
 #pragma unroll
               for (int i = 0; i < N; ++i) {
-                d[i] = delta ? x[i][e] : x[i][e] - b[e];
-                const bool keep = (kb[i] >> e) & 1u;
-                nzm |= (uint32_t)(keep && d[i] != 0.f) << i;
-                k[i] = keep ? d[i] * sr32[i] : 0.f;
+                const uint32_t xw = word_of(xw4[i], p);
+                const float2 x2 = make_float2(bf16_lo(xw), bf16_hi(xw));
+                const float2 d2 = delta ? x2 : __ffma2_rn(b2, neg1, x2);
+                const float2 m2 = make_float2(((kb[i] >> (2 * p)) & 1u) ? sr32[i] : 0.f,
+                                              ((kb[i] >> (2 * p + 1)) & 1u) ? sr32[i] : 0.f);
+                k2[i] = __fmul2_rn(d2, m2);
+                const bool zl = k2[i].x != 0.f, zh = k2[i].y != 0.f;
+                cnt_nz[i] += (uint32_t)zl + (uint32_t)zh;
+                nzl |= zl;
+                nzh |= zh;
+                aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
               }
-              bool slow = false;
+              bool sl = false, sh = false;
               if (N >= 2 && a.erase_mode) {
-                float vv = 0.f, A = 0.f;
+                float2 vv, gg;
                 if (a.erase_mode == 1) {
-                  vv = k[0];
-                  A = fabsf(k[0]);
+                  vv = k2[0];
 #pragma unroll
-                  for (int i = 1; i < N; ++i) { vv += k[i]; A += fabsf(k[i]); }
-                  slow = !(fabsf(vv) > 0x1p-20f * A);
+                  for (int i = 1; i < N; ++i) vv = __fadd2_rn(vv, k2[i]);
+                  gg = aa;
                 } else {
+                  vv = __fmul2_rn(k2[0], make_float2(fabsf(k2[0].x), fabsf(k2[0].y)));
+                  gg = __fmul2_rn(k2[0], k2[0]);
+#pragma unroll
+                  for (int i = 1; i < N; ++i) {
+                    vv = __ffma2_rn(k2[i], make_float2(fabsf(k2[i].x), fabsf(k2[i].y)), vv);
+                    gg = __ffma2_rn(k2[i], k2[i], gg);
+                  }
+                }
+                // |vote| must clear the certified error bound, unless every entry is exactly zero
+                sl = nzl && !(fabsf(vv.x) > cv * gg.x);
+                sh = nzh && !(fabsf(vv.y) > cv * gg.y);
+                const float2 sg = make_float2(copysignf(1.f, vv.x), copysignf(1.f, vv.y));
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                  const float2 t2 = __fmul2_rn(k2[i], sg);
+                  const bool ol = t2.x < 0.f, oh = t2.y < 0.f;
+                  cnt_er[i] += (uint32_t)ol + (uint32_t)oh;
+                  k2[i].x = ol ? 0.f : k2[i].x;
+                  k2[i].y = oh ? 0.f : k2[i].y;
+                }
+              }
+              float2 y2 = b2;
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                const float w = (float)a.w[i];
+                y2 = __ffma2_rn(make_float2(w, w), k2[i], y2);
+              }
+              // bf16 rounding decision must be certain: distance to the rounding midpoint > error bound
+              const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, make_float2(fabsf(b2.x), fabsf(b2.y)));
+              const float2 mid = make_float2(__uint_as_float((__float_as_uint(y2.x) & 0xffff0000u) | 0x8000u),
+                                             __uint_as_float((__float_as_uint(y2.y) & 0xffff0000u) | 0x8000u));
+              const float2 dm = __fadd2_rn(y2, make_float2(-mid.x, -mid.y));
+              sl = sl || !(fabsf(dm.x) > 0x1p-19f * S2.x);
+              sh = sh || !(fabsf(dm.y) > 0x1p-19f * S2.y);
+              slowm |= ((uint32_t)sl | ((uint32_t)sh << 1)) << (2 * p);
+              __nv_bfloat162 p2 = __floats2bfloat162_rn(y2.x, y2.y);
+              outw[p] = *reinterpret_cast<uint32_t*>(&p2);
+            }
+            // ---------------- phase 2 (rare): exact reference-order evaluation of flagged elements
+            if (slowm) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                if ((slowm >> e) & 1u) {
+                  const uint32_t bw = word_of(bw4, e >> 1);
+                  const float be = (e & 1) ? bf16_hi(bw) : bf16_lo(bw);
+                  FArr<N> xe;
+                  uint32_t keep = 0;
 #pragma unroll
                   for (int i = 0; i < N; ++i) {
-                    const float q2 = k[i] * k[i];
-                    vv += copysignf(q2, k[i]);
-                    A += q2;
+                    const uint32_t xw = word_of(xw4[i], e >> 1);
+                    xe.v[i] = (e & 1) ? bf16_hi(xw) : bf16_lo(xw);
+                    keep |= ((kb[i] >> e) & 1u) << i;
                   }
-                  slow = !(fabsf(vv) > 0x1p-19f * A);
+                  uint32_t nzm, erm;
+                  const double Y = merge_elem_slow<N>(be, xe, keep, &a, scale, &nzm, &erm);
+                  if (N >= 2 && a.erase_mode) {
+                    const uint32_t fo = fast_opp_bits<N>(be, xe.v, keep, sr32, a.erase_mode, delta);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) cnt_er[i] += ((erm >> i) & 1u) - ((fo >> i) & 1u);
+                  }
+                  const uint32_t hb = f64_to_bf16_rne(Y);
+                  uint32_t& w = outw[e >> 1];
+                  w = (e & 1) ? ((w & 0x0000ffffu) | (hb << 16)) : ((w & 0xffff0000u) | hb);
                 }
-                const uint32_t vs = __float_as_uint(vv) & 0x80000000u;
-#pragma unroll
-                for (int i = 0; i < N; ++i) {
-                  const bool opp = ((nzm >> i) & 1u) && ((__float_as_uint(d[i]) & 0x80000000u) != vs);
-                  if (opp) k[i] = 0.f;
-                  erm |= (uint32_t)opp << i;
-                }
               }
-              float yy = b[e], S = fabsf(b[e]);
-#pragma unroll
-              for (int i = 0; i < N; ++i) {
-                yy = fmaf(w32[i], k[i], yy);
-                S = fmaf(w32[i], fabsf(k[i]), S);
-              }
-              const float mid = __uint_as_float((__float_as_uint(yy) & 0xffff0000u) | 0x8000u);
-              slow = slow || !(fabsf(yy - mid) > 0x1p-19f * S);
-              y[e] = yy;
-              if (slow) {
-                // certified guard tripped: exact reference-order evaluation of this element
-                double X[N];
-                uint32_t keep = 0;
-#pragma unroll
-                for (int i = 0; i < N; ++i) {
-                  X[i] = (double)x[i][e];
-                  keep |= ((kb[i] >> e) & 1u) << i;
-                }
-                const double Y = merge_elem_f64<N>((double)b[e], X, keep, a, c, nzm, erm);
-                slowbits[e] = f64_to_bf16_rne(Y);
-                slowmask |= 1u << e;
-              }
-#pragma unroll
-              for (int i = 0; i < N; ++i) {
-                cnt_nz[i] += (nzm >> i) & 1u;
-                cnt_er[i] += (erm >> i) & 1u;
-              }
-            }
-            uint32_t outw[4];
-#pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) {
-              __nv_bfloat162 p2 = __floats2bfloat162_rn(y[2 * e2], y[2 * e2 + 1]);
-              uint32_t w = *reinterpret_cast<uint32_t*>(&p2);
-              if (slowmask & (1u << (2 * e2))) w = (w & 0xffff0000u) | slowbits[2 * e2];
-              if (slowmask & (2u << (2 * e2))) w = (w & 0x0000ffffu) | (slowbits[2 * e2 + 1] << 16);
-              outw[e2] = w;
             }
             stg128_stream((uint16_t*)g.seg->out + out_base + le, make_uint4(outw[0], outw[1], outw[2], outw[3]));
-            continue;
           }
         }
-        // ---- generic f64 path (reference operation order)
-        double b[VEC], x[N][VEC];
-        if (wb) VecIO<DTI>::f64(lds128(sb + v * 16), b);
-        else {
+      } else {
+        // ---------------- reference-order f64 path
+        for (uint32_t v = tid; v < nvec; v += kCThreads) {
+          const uint32_t le = v * VEC;
+          double b[VEC], x[N][VEC];
+          if (wb) VecIO<DTI>::f64(lds128(sb + v * 16), b);
+          else {
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) b[e] = 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < N; ++i) VecIO<DTI>::f64(lds128(sb + (i + (wb ? 1 : 0)) * SB + v * 16), x[i]);
-        double y[VEC];
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          double X[N];
-#pragma unroll
-          for (int i = 0; i < N; ++i) X[i] = x[i][e];
-          const uint32_t keep = keep_bits_for<N, VEC>(a, bm, BMB, le, jtensor0 + off + le, e);
-          uint32_t nzm, erm;
-          y[e] = merge_elem_f64<N>(b[e], X, keep, a, c, nzm, erm);
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            cnt_nz[i] += (nzm >> i) & 1u;
-            cnt_er[i] += (erm >> i) & 1u;
+            for (int e = 0; e < VEC; ++e) b[e] = 0.0;
           }
+#pragma unroll
+          for (int i = 0; i < N; ++i) VecIO<DTI>::f64(lds128(sb + (i + (wb ? 1 : 0)) * SB + v * 16), x[i]);
+          double y[VEC];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            double X[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) X[i] = x[i][e];
+            const uint32_t keep = keep_bits_for<N, VEC>(a, bm, BMB, le, jtensor0 + off + le, e);
+            uint32_t nzm, erm;
+            y[e] = merge_elem_f64<N>(b[e], X, keep, a, c, nzm, erm);
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              cnt_nz[i] += (nzm >> i) & 1u;
+              cnt_er[i] += (erm >> i) & 1u;
+            }
+          }
+          store_vec_f64<DTO, VEC>(g.seg->out, out_base + le, y);
         }
-        store_vec_f64<DTO, VEC>(g.seg->out, out_base + le, y);
       }
       // tail elements (fewer than 16 bytes) straight from global memory
       for (uint32_t e = main_elems + tid; e < n; e += kCThreads) {
@@ -640,7 +712,8 @@ static int launch_merge(MergeArgs& a, cudaStream_t s) {
   a.stage_bytes = sb;
   a.nstages = ns;
   const uint32_t smem = 1024 + sb * ns;
-  auto kern = k_merge<DTI, DTO, N>;
+  constexpr bool kFastable = (DTI == RLK_BF16 && DTO == RLK_BF16);
+  auto kern = (kFastable && a.fast) ? k_merge<DTI, DTO, N, kFastable> : k_merge<DTI, DTO, N, false>;
   int st = ensure_smem(kern, smem);
   if (st) return st;
   uint32_t grid = std::min<uint32_t>(a.plan.n_items, (uint32_t)sm_count());

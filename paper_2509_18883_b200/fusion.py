@@ -224,6 +224,25 @@ class FusionCall:
         self.keep_prob = 1.0 - p
         self.bitmap = None
         self.words_per_row = 0
+        self.timers: dict[str, list] | None = None  # name -> [(start_event, end_event)] when profiling
+
+    def _launch(self, name: str, *args) -> None:
+        if self.timers is None:
+            L.call(name, *args)
+            return
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
+        L.call(name, *args)
+        e1.record(self.stream)
+        self.timers.setdefault(name, []).append((e0, e1))
+
+    def run(self, weights: Sequence[float], dtype_out: torch.dtype | None = None) -> "FusionCall":
+        """One complete fusion step on the call's stream: zero counters, K1, [all_reduce], finalize,
+        [K2], K3.  Reusing a FusionCall across steps reuses its launch plan (host metadata only)."""
+        with torch.cuda.stream(self.stream):
+            self.counters.zero_()
+        return self.norms().merge(weights, dtype_out)
 
     # -- K1 + all_reduce + finalize
     def norms(self, precomputed_sumsq: torch.Tensor | None = None) -> "FusionCall":
@@ -234,15 +253,17 @@ class FusionCall:
                 if self.group is not None:
                     import torch.distributed as dist
                     world = dist.get_world_size(self.group)
-                alloc = torch.zeros if world > 1 else torch.empty
-                self.partials = alloc(self.layout.n_items * self.n, dtype=torch.float64, device=self.device)
-                L.call("rlk_fusion_sumsq", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
-                       int(self.delta_mode), L.ptr(self.partials), s)
+                if self.partials is None or self.partials.numel() != self.layout.n_items * self.n:
+                    self.partials = torch.zeros(self.layout.n_items * self.n, dtype=torch.float64, device=self.device)
+                elif world > 1:
+                    self.partials.zero_()  # other ranks' slots must be exactly zero for the exact sum
+                self._launch("rlk_fusion_sumsq", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
+                             int(self.delta_mode), L.ptr(self.partials), s)
                 if world > 1:
                     import torch.distributed as dist
                     # disjoint slots: the sum is exact, so norms are identical at every world size
                     dist.all_reduce(self.partials, op=dist.ReduceOp.SUM, group=self.group)
-                L.call("rlk_fusion_finalize", L.ptr(self.partials),
+                self._launch("rlk_fusion_finalize", L.ptr(self.partials),
                        L.ptr(self.layout.tensor_items_device(self.device)), self.layout.n_tensors, self.n,
                        self.cfg.target_mode, float(self.cfg.target_norm) if self.cfg.target_mode == 2 else 0.0,
                        L.ptr(self.sumsq), L.ptr(self.scale), L.ptr(self.status), s)
@@ -270,15 +291,16 @@ class FusionCall:
             if self.dropout_mode == 2:
                 n_bits = ((self.plan.max_extent + 8191) // 8192) * 8192
                 self.words_per_row = n_bits // 32
-                self.bitmap = torch.empty(self.n * self.words_per_row, dtype=torch.int32, device=self.device)
+                if self.bitmap is None or self.bitmap.numel() != self.n * self.words_per_row:
+                    self.bitmap = torch.empty(self.n * self.words_per_row, dtype=torch.int32, device=self.device)
                 seeds = (L.C.c_uint64 * self.n)(*self.seeds)
-                L.call("rlk_fusion_mask_bitmap", seeds, self.n, self.thresh, n_bits, L.ptr(self.bitmap),
-                       self.words_per_row, s)
+                self._launch("rlk_fusion_mask_bitmap", seeds, self.n, self.thresh, n_bits, L.ptr(self.bitmap),
+                             self.words_per_row, s)
             w = (L.C.c_double * self.n)(*[float(x) for x in weights])
             seeds = (L.C.c_uint64 * self.n)(*self.seeds)
             dmode = (1 | (2 if self.with_base else 0)) if self.delta_mode else 0
             dto = dtype_out or self.pieces[0].out.dtype
-            L.call("rlk_fusion_merge", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
+            self._launch("rlk_fusion_merge", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
                    L.dtype_code(dto), dmode, L.ptr(self.scale), w, self.dropout_mode,
                    seeds if self.dropout_mode else None, self.thresh, self.keep_prob,
                    L.ptr(self.bitmap), self.words_per_row, erase, L.ptr(self.counters), s)

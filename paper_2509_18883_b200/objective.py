@@ -204,6 +204,13 @@ class GRPOBatch:
     def n_rows(self) -> int:
         return int(self.tokens.numel())
 
+    def all_groups_seg(self) -> torch.Tensor:
+        seg = getattr(self, "_all_seg", None)
+        if seg is None:
+            seg = torch.tensor([0, self.n_groups], dtype=torch.int64, device=self.tokens.device)
+            self._all_seg = seg
+        return seg
+
     @staticmethod
     def pack(tokens, logp_train, logp_infer, cu_seqlens, adv, use, group_size: int, t_max: int,
              temperature=1.0, device=None, row_index=None) -> "GRPOBatch":
@@ -252,6 +259,9 @@ def grpo_forward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = Clip
     rank's share and the per-group sums are all-reduced (one f64 vector)."""
     if logits.ndim != 2:
         raise ValueError("logits must be [rows, vocab]")
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return grpo_forward(logits, batch, clip, group=group)
     logits = logits.contiguous()
     R, V = batch.n_rows, logits.shape[1]
     dev = logits.device
@@ -271,14 +281,16 @@ def grpo_forward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = Clip
         dist.all_reduce(gs, group=group)
     scaled = gs / float(batch.group_size * batch.t_max)
     tot = torch.empty(1, **f64)
-    seg = torch.tensor([0, batch.n_groups], dtype=torch.int64, device=dev)
-    L.call("rlk_segment_sum_f64", L.ptr(scaled), L.ptr(seg), 1, L.ptr(tot), s)
+    L.call("rlk_segment_sum_f64", L.ptr(scaled), L.ptr(batch.all_groups_seg()), 1, L.ptr(tot), s)
     return GRPOForward(tot[0] / batch.n_groups, gs, logp, lse, term, coef, flags)
 
 
 def grpo_backward(logits: torch.Tensor, batch: GRPOBatch, fwd: GRPOForward, grad_scale: torch.Tensor | float = 1.0,
                   grad_dtype: torch.dtype | None = None, *, stream=None) -> torch.Tensor:
     """K5: dJ/dlogits for one-row-per-token batches, scaled by `grad_scale` (the autograd grad_out)."""
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return grpo_backward(logits, batch, fwd, grad_scale, grad_dtype)
     R, V = logits.shape
     coef = fwd.coef if (isinstance(grad_scale, float) and grad_scale == 1.0) else fwd.coef * grad_scale
     coef = coef.contiguous()
