@@ -437,8 +437,8 @@ __device__ __forceinline__ uint32_t word_of(const uint4& q, int p) {
   return p == 0 ? q.x : (p == 1 ? q.y : (p == 2 ? q.z : q.w));
 }
 
-// FAST: bf16 -> bf16 with the f32x2 fast path; otherwise the reference-order f64 path only.
-template <int DTI, int DTO, int N, bool FAST>
+// Generic K3: the reference-order f64 path for every dtype combination (and the tails).
+template <int DTI, int DTO, int N>
 __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ MergeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DTI>::size;
@@ -460,17 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
     const ItemGeom g = item_geom(a.plan, item);
     const double* scale = a.scale + (uint64_t)g.tensor * N;
     ElemConsts c;
-    float sr32[N];
-    float wmax = 0.f;
-    bool fast_ok = FAST;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      c.scale[i] = __ldg(scale + i);
-      sr32[i] = (float)(a.dropout_mode ? c.scale[i] / a.keep_prob : c.scale[i]);
-      wmax = fmaxf(wmax, (float)a.w[i]);
-      // k = d * sr cannot underflow for bf16 deltas (|d| >= 2^-133) when sr >= 2^-16
-      fast_ok = fast_ok && sr32[i] >= 0x1p-16f && sr32[i] < 0x1p100f;
-    }
+    for (int i = 0; i < N; ++i) c.scale[i] = __ldg(scale + i);
     uint32_t cnt_nz[N], cnt_er[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) cnt_nz[i] = cnt_er[i] = 0;
@@ -484,129 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
       const uint8_t* bm = sb + (N + 1) * SB;
       const uint32_t nvec = main_elems / VEC;
       const uint64_t out_base = g.start + off;
-      if (FAST && fast_ok) {
-        if constexpr (FAST) {
-          // ---------------- phase 1: branch-free, two elements per f32x2 op
-          const float2 neg1 = make_float2(-1.f, -1.f);
-          const float cv = a.erase_mode == 1 ? 0x1p-20f : 0x1p-19f;
-          for (uint32_t v = tid; v < nvec; v += kCThreads) {
-            const uint32_t le = v * 8;
-            const uint4 bw4 = wb ? lds128(sb + v * 16) : make_uint4(0, 0, 0, 0);
-            uint4 xw4[N];
-            uint32_t kb[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-              xw4[i] = lds128(sb + (i + (wb ? 1 : 0)) * SB + v * 16);
-              if (a.dropout_mode == 2) kb[i] = bm[i * BMB + (le >> 3)];
-              else if (a.dropout_mode == 1) {
-                kb[i] = 0;
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  kb[i] |= (uint32_t)keep_draw(a.seed[i], jtensor0 + off + le + e, a.thresh) << e;
-              } else kb[i] = 0xffu;
-            }
-            uint32_t outw[4];
-            uint32_t slowm = 0;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              const uint32_t bw = word_of(bw4, p);
-              const float2 b2 = make_float2(bf16_lo(bw), bf16_hi(bw));
-              float2 k2[N];
-              float2 aa = make_float2(0.f, 0.f);
-              bool nzl = false, nzh = false;
-#pragma unroll
-              for (int i = 0; i < N; ++i) {
-                const uint32_t xw = word_of(xw4[i], p);
-                const float2 x2 = make_float2(bf16_lo(xw), bf16_hi(xw));
-                const float2 d2 = delta ? x2 : __ffma2_rn(b2, neg1, x2);
-                const float2 m2 = make_float2(((kb[i] >> (2 * p)) & 1u) ? sr32[i] : 0.f,
-                                              ((kb[i] >> (2 * p + 1)) & 1u) ? sr32[i] : 0.f);
-                k2[i] = __fmul2_rn(d2, m2);
-                const bool zl = k2[i].x != 0.f, zh = k2[i].y != 0.f;
-                cnt_nz[i] += (uint32_t)zl + (uint32_t)zh;
-                nzl |= zl;
-                nzh |= zh;
-                aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
-              }
-              bool sl = false, sh = false;
-              if (N >= 2 && a.erase_mode) {
-                float2 vv, gg;
-                if (a.erase_mode == 1) {
-                  vv = k2[0];
-#pragma unroll
-                  for (int i = 1; i < N; ++i) vv = __fadd2_rn(vv, k2[i]);
-                  gg = aa;
-                } else {
-                  vv = __fmul2_rn(k2[0], make_float2(fabsf(k2[0].x), fabsf(k2[0].y)));
-                  gg = __fmul2_rn(k2[0], k2[0]);
-#pragma unroll
-                  for (int i = 1; i < N; ++i) {
-                    vv = __ffma2_rn(k2[i], make_float2(fabsf(k2[i].x), fabsf(k2[i].y)), vv);
-                    gg = __ffma2_rn(k2[i], k2[i], gg);
-                  }
-                }
-                // |vote| must clear the certified error bound, unless every entry is exactly zero
-                sl = nzl && !(fabsf(vv.x) > cv * gg.x);
-                sh = nzh && !(fabsf(vv.y) > cv * gg.y);
-                const float2 sg = make_float2(copysignf(1.f, vv.x), copysignf(1.f, vv.y));
-#pragma unroll
-                for (int i = 0; i < N; ++i) {
-                  const float2 t2 = __fmul2_rn(k2[i], sg);
-                  const bool ol = t2.x < 0.f, oh = t2.y < 0.f;
-                  cnt_er[i] += (uint32_t)ol + (uint32_t)oh;
-                  k2[i].x = ol ? 0.f : k2[i].x;
-                  k2[i].y = oh ? 0.f : k2[i].y;
-                }
-              }
-              float2 y2 = b2;
-#pragma unroll
-              for (int i = 0; i < N; ++i) {
-                const float w = (float)a.w[i];
-                y2 = __ffma2_rn(make_float2(w, w), k2[i], y2);
-              }
-              // bf16 rounding decision must be certain: distance to the rounding midpoint > error bound
-              const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, make_float2(fabsf(b2.x), fabsf(b2.y)));
-              const float2 mid = make_float2(__uint_as_float((__float_as_uint(y2.x) & 0xffff0000u) | 0x8000u),
-                                             __uint_as_float((__float_as_uint(y2.y) & 0xffff0000u) | 0x8000u));
-              const float2 dm = __fadd2_rn(y2, make_float2(-mid.x, -mid.y));
-              sl = sl || !(fabsf(dm.x) > 0x1p-19f * S2.x);
-              sh = sh || !(fabsf(dm.y) > 0x1p-19f * S2.y);
-              slowm |= ((uint32_t)sl | ((uint32_t)sh << 1)) << (2 * p);
-              __nv_bfloat162 p2 = __floats2bfloat162_rn(y2.x, y2.y);
-              outw[p] = *reinterpret_cast<uint32_t*>(&p2);
-            }
-            // ---------------- phase 2 (rare): exact reference-order evaluation of flagged elements
-            if (slowm) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                if ((slowm >> e) & 1u) {
-                  const uint32_t bw = word_of(bw4, e >> 1);
-                  const float be = (e & 1) ? bf16_hi(bw) : bf16_lo(bw);
-                  FArr<N> xe;
-                  uint32_t keep = 0;
-#pragma unroll
-                  for (int i = 0; i < N; ++i) {
-                    const uint32_t xw = word_of(xw4[i], e >> 1);
-                    xe.v[i] = (e & 1) ? bf16_hi(xw) : bf16_lo(xw);
-                    keep |= ((kb[i] >> e) & 1u) << i;
-                  }
-                  uint32_t nzm, erm;
-                  const double Y = merge_elem_slow<N>(be, xe, keep, &a, scale, &nzm, &erm);
-                  if (N >= 2 && a.erase_mode) {
-                    const uint32_t fo = fast_opp_bits<N>(be, xe.v, keep, sr32, a.erase_mode, delta);
-#pragma unroll
-                    for (int i = 0; i < N; ++i) cnt_er[i] += ((erm >> i) & 1u) - ((fo >> i) & 1u);
-                  }
-                  const uint32_t hb = f64_to_bf16_rne(Y);
-                  uint32_t& w = outw[e >> 1];
-                  w = (e & 1) ? ((w & 0x0000ffffu) | (hb << 16)) : ((w & 0xffff0000u) | hb);
-                }
-              }
-            }
-            stg128_stream((uint16_t*)g.seg->out + out_base + le, make_uint4(outw[0], outw[1], outw[2], outw[3]));
-          }
-        }
-      } else {
+      {
         // ---------------- reference-order f64 path
         for (uint32_t v = tid; v < nvec; v += kCThreads) {
           const uint32_t le = v * VEC;
@@ -675,6 +544,217 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
   }
 }
 
+
+__device__ __forceinline__ uint32_t mask_ne0(float x) {  // 0xffffffff iff x != 0
+  uint32_t r;
+  asm("set.ne.u32.f32 %0, %1, 0f00000000;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t mask_lt0(float x) {  // 0xffffffff iff x < 0 (false for -0)
+  uint32_t r;
+  asm("set.lt.u32.f32 %0, %1, 0f00000000;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float andnot_f(float x, uint32_t m) { return __uint_as_float(__float_as_uint(x) & ~m); }
+
+// Fast K3 for bf16 experts + bf16 base -> bf16 (the checkpoint path): f32x2 arithmetic with certified
+// guards; DROP 0 = no dropout, 2 = keep bits from the K2 bitmap; ERASE 0 off, 1 sum vote, 2 squared vote.
+// Elements whose guard trips are recomputed exactly (merge_elem_slow) in a rarely-taken phase 2.
+template <int N, int DROP, int ERASE>
+__global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constant__ MergeArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr uint32_t SB = StreamBytes<N>::v;
+  constexpr uint32_t ELEMS = SB / 2;
+  constexpr uint32_t BMB = ELEMS / 8;
+  constexpr bool kErase = (ERASE != 0) && (N >= 2);
+  const Ring r = ring_setup(smem, a.stage_bytes, a.nstages);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == kCWarps) {
+    if (lane == 0) produce<2, N>(a.plan, r, true, DROP == 2 ? a.bitmap : nullptr, a.words_per_row);
+    return;
+  }
+  const int tid = threadIdx.x;
+  const float cv = ERASE == 1 ? 0x1p-20f : 0x1p-19f;
+  float w32[N];
+  float wmax = 0.f;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    w32[i] = (float)a.w[i];
+    wmax = fmaxf(wmax, w32[i]);
+  }
+  uint32_t q = 0;
+  for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
+    const ItemGeom g = item_geom(a.plan, item);
+    const double* scale = a.scale + (uint64_t)g.tensor * N;
+    uint16_t* const outp = (uint16_t*)g.seg->out;
+    ElemConsts c;
+    float sr32[N];
+    bool fast_ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      c.scale[i] = __ldg(scale + i);
+      sr32[i] = (float)(DROP ? c.scale[i] / a.keep_prob : c.scale[i]);
+      // k = d * sr cannot underflow for bf16 deltas (|d| >= 2^-133) when sr >= 2^-16
+      fast_ok = fast_ok && sr32[i] >= 0x1p-16f && sr32[i] < 0x1p100f;
+    }
+    uint32_t cnt_nz[N], cnt_er[N];  // counted negatively through all-ones masks
+#pragma unroll
+    for (int i = 0; i < N; ++i) cnt_nz[i] = cnt_er[i] = 0;
+    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    for (uint32_t off = 0; off < g.len; off += ELEMS) {
+      const uint32_t n = min(ELEMS, g.len - off);
+      const uint32_t main_elems = ((n * 2) & ~15u) / 2;
+      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      mbar_wait(&r.full[s], ph);
+      const uint8_t* sb = r.buf + s * r.stage_bytes;
+      const uint8_t* bm = sb + (N + 1) * SB;
+      const uint32_t nvec = main_elems / 8;
+      const uint64_t out_base = g.start + off;
+      for (uint32_t v = fast_ok ? tid : nvec; v < nvec; v += kCThreads) {
+        const uint32_t le = v * 8;
+        const uint4 bw4 = lds128(sb + v * 16);
+        uint4 xw4[N];
+        uint32_t kb[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          xw4[i] = lds128(sb + (i + 1) * SB + v * 16);
+          kb[i] = DROP ? (uint32_t)bm[i * BMB + v] : 0xffu;
+        }
+        uint32_t outw[4];
+        uint32_t slowm = 0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint32_t bw = word_of(bw4, p);
+          const float2 b2 = make_float2(bf16_lo(bw), bf16_hi(bw));
+          float2 k2[N];
+          float2 aa = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            const uint32_t xw = word_of(xw4[i], p);
+            const float2 d2 = __ffma2_rn(b2, make_float2(-1.f, -1.f), make_float2(bf16_lo(xw), bf16_hi(xw)));
+            if (DROP) {
+              const float2 m2 = make_float2(((kb[i] >> (2 * p)) & 1u) ? sr32[i] : 0.f,
+                                            ((kb[i] >> (2 * p + 1)) & 1u) ? sr32[i] : 0.f);
+              k2[i] = __fmul2_rn(d2, m2);
+            } else {
+              k2[i] = __fmul2_rn(d2, make_float2(sr32[i], sr32[i]));
+            }
+            cnt_nz[i] -= mask_ne0(k2[i].x);
+            cnt_nz[i] -= mask_ne0(k2[i].y);
+            aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
+          }
+          bool sl = false, sh = false;
+          if constexpr (kErase) {
+            float2 vv, gg;
+            if (ERASE == 1) {
+              vv = k2[0];
+#pragma unroll
+              for (int i = 1; i < N; ++i) vv = __fadd2_rn(vv, k2[i]);
+              gg = aa;
+            } else {
+              vv = __fmul2_rn(k2[0], make_float2(fabsf(k2[0].x), fabsf(k2[0].y)));
+              gg = __fmul2_rn(k2[0], k2[0]);
+#pragma unroll
+              for (int i = 1; i < N; ++i) {
+                vv = __ffma2_rn(k2[i], make_float2(fabsf(k2[i].x), fabsf(k2[i].y)), vv);
+                gg = __ffma2_rn(k2[i], k2[i], gg);
+              }
+            }
+            // |vote| must clear the certified error bound (an all-zero column is an exact tie)
+            sl = (gg.x > 0.f) && !(fabsf(vv.x) > cv * gg.x);
+            sh = (gg.y > 0.f) && !(fabsf(vv.y) > cv * gg.y);
+            const float2 sg = make_float2(copysignf(1.f, vv.x), copysignf(1.f, vv.y));
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              const float2 t2 = __fmul2_rn(k2[i], sg);
+              const uint32_t ml = mask_lt0(t2.x), mh = mask_lt0(t2.y);
+              cnt_er[i] -= ml;
+              cnt_er[i] -= mh;
+              k2[i] = make_float2(andnot_f(k2[i].x, ml), andnot_f(k2[i].y, mh));
+            }
+          }
+          float2 y2 = b2;
+#pragma unroll
+          for (int i = 0; i < N; ++i) y2 = __ffma2_rn(make_float2(w32[i], w32[i]), k2[i], y2);
+          // bf16 rounding must be certain: distance to the rounding midpoint > error bound
+          const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, make_float2(fabsf(b2.x), fabsf(b2.y)));
+          const float2 mid = make_float2(__uint_as_float((__float_as_uint(y2.x) & 0xffff0000u) | 0x8000u),
+                                         __uint_as_float((__float_as_uint(y2.y) & 0xffff0000u) | 0x8000u));
+          const float2 dm = __fadd2_rn(y2, make_float2(-mid.x, -mid.y));
+          sl = sl || !(fabsf(dm.x) > 0x1p-19f * S2.x);
+          sh = sh || !(fabsf(dm.y) > 0x1p-19f * S2.y);
+          slowm |= ((uint32_t)sl | ((uint32_t)sh << 1)) << (2 * p);
+          __nv_bfloat162 p2 = __floats2bfloat162_rn(y2.x, y2.y);
+          outw[p] = *reinterpret_cast<uint32_t*>(&p2);
+        }
+        if (slowm) {  // phase 2 (rare): exact reference-order evaluation of flagged elements
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if ((slowm >> e) & 1u) {
+              const uint32_t bw = word_of(bw4, e >> 1);
+              const float be = (e & 1) ? bf16_hi(bw) : bf16_lo(bw);
+              FArr<N> xe;
+              uint32_t keep = 0;
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                const uint32_t xw = word_of(xw4[i], e >> 1);
+                xe.v[i] = (e & 1) ? bf16_hi(xw) : bf16_lo(xw);
+                keep |= ((kb[i] >> e) & 1u) << i;
+              }
+              uint32_t nzm, erm;
+              const double Y = merge_elem_slow<N>(be, xe, keep, &a, scale, &nzm, &erm);
+              if constexpr (kErase) {
+                const uint32_t fo = fast_opp_bits<N>(be, xe.v, keep, sr32, ERASE, false);
+#pragma unroll
+                for (int i = 0; i < N; ++i) cnt_er[i] -= ((fo >> i) & 1u) - ((erm >> i) & 1u);
+              }
+              const uint32_t hb = f64_to_bf16_rne(Y);
+              uint32_t& w = outw[e >> 1];
+              w = (e & 1) ? ((w & 0x0000ffffu) | (hb << 16)) : ((w & 0xffff0000u) | hb);
+            }
+          }
+        }
+        stg128_stream(outp + out_base + le, make_uint4(outw[0], outw[1], outw[2], outw[3]));
+      }
+      // items the fast path cannot certify, and the < 16-byte tail: exact f64 path
+      const uint32_t e0 = fast_ok ? main_elems : 0;
+      for (uint32_t e = e0 + tid; e < n; e += kCThreads) {
+        const uint64_t idx = g.start + off + e;
+        const double B = load_f64<RLK_BF16>(g.seg->base, idx);
+        double X[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) X[i] = load_f64<RLK_BF16>(g.seg->expert[i], idx);
+        uint32_t keep = (1u << N) - 1u;
+        if (DROP) {
+          keep = 0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) keep |= (uint32_t)keep_draw(a.seed[i], jtensor0 + off + e, a.thresh) << i;
+        }
+        uint32_t nzm, erm;
+        const double Y = merge_elem_f64<N>(B, X, keep, a, c, nzm, erm);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          cnt_nz[i] -= 0u - ((nzm >> i) & 1u);
+          cnt_er[i] -= 0u - ((erm >> i) & 1u);
+        }
+        store_from_f64<RLK_BF16>(g.seg->out, idx, Y);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r.empty[s]);
+      ++q;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint32_t z = __reduce_add_sync(0xffffffffu, cnt_nz[i]);
+      const uint32_t er = __reduce_add_sync(0xffffffffu, cnt_er[i]);
+      if (lane == 0) {
+        if (z) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + i, (unsigned long long)z);
+        if (er) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + N + i, (unsigned long long)er);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host-side launch helpers
 template <int N>
 static void stage_geometry(int esz, bool bitmap, uint32_t& stage_bytes, uint32_t& nstages) {
@@ -705,15 +785,41 @@ static int launch_sumsq(const rlk_fusion_plan& plan, int delta, double* partials
   return launch_status("rlk_fusion_sumsq");
 }
 
+template <int N, int DROP, int ERASE>
+static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
+  const uint32_t smem = 1024 + a.stage_bytes * a.nstages;
+  auto kern = k_merge_fast<N, DROP, ERASE>;
+  int st = ensure_smem(kern, smem);
+  if (st) return st;
+  uint32_t grid = std::min<uint32_t>(a.plan.n_items, (uint32_t)sm_count());
+  kern<<<grid, kThreads, smem, s>>>(a);
+  return launch_status("rlk_fusion_merge");
+}
+
+template <int N>
+static int dispatch_fast(MergeArgs& a, cudaStream_t s) {
+  const int ec = N >= 2 ? a.erase_mode : 0;
+  if (a.dropout_mode == 2) {
+    if (ec == 1) return launch_merge_fast<N, 2, 1>(a, s);
+    if (ec == 2) return launch_merge_fast<N, 2, 2>(a, s);
+    return launch_merge_fast<N, 2, 0>(a, s);
+  }
+  if (ec == 1) return launch_merge_fast<N, 0, 1>(a, s);
+  if (ec == 2) return launch_merge_fast<N, 0, 2>(a, s);
+  return launch_merge_fast<N, 0, 0>(a, s);
+}
+
 template <int DTI, int DTO, int N>
 static int launch_merge(MergeArgs& a, cudaStream_t s) {
   uint32_t sb, ns;
   stage_geometry<N>(Elem<DTI>::size, a.dropout_mode == 2, sb, ns);
   a.stage_bytes = sb;
   a.nstages = ns;
+  if constexpr (DTI == RLK_BF16 && DTO == RLK_BF16 && N <= 4) {
+    if (a.fast && !a.delta_mode && a.with_base && a.dropout_mode != 1) return dispatch_fast<N>(a, s);
+  }
   const uint32_t smem = 1024 + sb * ns;
-  constexpr bool kFastable = (DTI == RLK_BF16 && DTO == RLK_BF16);
-  auto kern = (kFastable && a.fast) ? k_merge<DTI, DTO, N, kFastable> : k_merge<DTI, DTO, N, false>;
+  auto kern = k_merge<DTI, DTO, N>;
   int st = ensure_smem(kern, smem);
   if (st) return st;
   uint32_t grid = std::min<uint32_t>(a.plan.n_items, (uint32_t)sm_count());

@@ -216,8 +216,10 @@ class FusionCall:
         if p == 0.0:
             dropout_mode = 0
         elif dropout_mode not in (1, 2):
-            # K2 bitmap pays N * max_extent draws once; inline hashing pays N per element in K3.
-            dropout_mode = 2 if self.plan.local_elems >= 2 * self.plan.max_extent else 1
+            # K2 bitmap pays N * max_extent draws once; inline hashing pays N per element in K3.  The
+            # bf16 fast merge path reads keep bits from the bitmap only.
+            dropout_mode = 2 if (self.plan.local_elems >= 2 * self.plan.max_extent
+                                 or self.dtype_in == torch.bfloat16) else 1
         self.dropout_mode = dropout_mode
         self.seeds = fusion_child_seeds(cfg.seed, n_experts) if p > 0 else [0] * n_experts
         self.thresh = keep_threshold(p) if p > 0 else 0
