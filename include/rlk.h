@@ -74,9 +74,15 @@ int rlk_abi_version(void);
 int rlk_device_sm_count(int device);
 
 /* K1: partials[(item0 + k) * n_experts + i] = sum over item k of (expert_i - base)^2 in f64 (or
- * delta_i^2).  Non-finite inputs propagate into the partial (detected by rlk_fusion_finalize). */
+ * delta_i^2).  Non-finite inputs propagate into the partial (detected by rlk_fusion_finalize).
+ * With nz_counters (device [n_tensors * 2N] u64, accumulated) it also counts, per (tensor, expert),
+ * the entries that are non-zero after dropout (FusionStats.dropout_kept_fraction numerator,
+ * fusion.py:172-174); the keep bits come from the K2 bitmap (dropout_mode 2), inline SplitMix64
+ * (1, child_seeds a HOST array) or none (0), so K2 runs before K1. */
 int rlk_fusion_sumsq(const rlk_fusion_plan* plan, int n_experts, int dtype, int delta_mode,
-                     double* partials, void* stream);
+                     double* partials, unsigned long long* nz_counters, int dropout_mode,
+                     const uint64_t* child_seeds, uint64_t thresh, const uint32_t* bitmap,
+                     uint64_t words_per_row, void* stream);
 
 /* Per tensor t: sumsq[t*N+i] = sum of its item partials in a fixed order (items
  * tensor_items[t] .. tensor_items[t+1]-1); norm = sqrt(sumsq); target per target_mode
@@ -97,8 +103,8 @@ int rlk_fusion_mask_bitmap(const uint64_t* child_seeds, int n_experts, uint64_t 
  * scale: device [n_tensors * N] f64 (from finalize).  weights / child_seeds: HOST arrays.
  * dropout_mode: 0 none, 1 inline SplitMix64, 2 bitmap (bitmap/words_per_row from K2).
  * keep_prob = 1 - p (f64, as the reference computes it).  erase_mode: 0 off, 1 sum, 2 squared.
- * counters: device [n_tensors * 2N] u64, accumulated (caller zeroes): [t*2N + i] = non-zero entries
- * after dropout, [t*2N + N + i] = entries erased. */
+ * counters: device [n_tensors * 2N] u64, accumulated (caller zeroes): K3 adds the entries erased at
+ * [t*2N + N + i] (the non-zero-after-dropout counts at [t*2N + i] come from K1). */
 int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, int dtype_out,
                      int delta_mode, const double* scale, const double* weights, int dropout_mode,
                      const uint64_t* child_seeds, uint64_t thresh, double keep_prob,

@@ -50,7 +50,7 @@ SIGNATURES = {
     "rlk_last_error": (C.c_char_p, []),
     "rlk_abi_version": (_I, []),
     "rlk_device_sm_count": (_I, [_I]),
-    "rlk_fusion_sumsq": (_I, [C.POINTER(FusionPlanC), _I, _I, _I, _P, _P]),
+    "rlk_fusion_sumsq": (_I, [C.POINTER(FusionPlanC), _I, _I, _I, _P, _P, _I, _P, _U64, _P, _U64, _P]),
     "rlk_fusion_finalize": (_I, [_P, _P, C.c_uint32, _I, _I, _D, _P, _P, _P, _P]),
     "rlk_fusion_mask_bitmap": (_I, [_P, _I, _U64, _U64, _P, _U64, _P]),
     "rlk_fusion_merge": (_I, [C.POINTER(FusionPlanC), _I, _I, _I, _I, _P, _P, _I, _P, _U64, _D, _P, _U64, _I,

@@ -166,49 +166,83 @@ __device__ __forceinline__ void store_vec_f64(void* out, uint64_t idx, const dou
   }
 }
 
-// ------------------------------------------------------------------ K1: norm partials
+// ------------------------------------------------------------------ K1: norm partials (+ non-zero counts)
+struct SumsqArgs {
+  rlk_fusion_plan plan;
+  double* partials;
+  unsigned long long* counters;  // nullable: [t*2N + i] += non-zero entries after dropout
+  const uint32_t* bitmap;        // dropout_mode 2
+  uint64_t words_per_row;
+  uint64_t seed[RLK_MAX_EXPERTS];
+  uint64_t thresh;
+  int delta_mode, dropout_mode;
+  uint32_t stage_bytes, nstages;
+};
+
+// Two CTAs per SM: the loop is bound by F2F (XU pipe) and fp64 latency, so it needs the warps.
 template <int DT, int N>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_sumsq(rlk_fusion_plan plan, int delta_mode, double* __restrict__ partials, uint32_t stage_bytes,
-            uint32_t nstages) {
+__global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ SumsqArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DT>::size;
   constexpr int VEC = 16 / ESZ;
   constexpr uint32_t SB = StreamBytes<N>::v;
   constexpr uint32_t ELEMS = SB / ESZ;
-  const Ring r = ring_setup(smem, stage_bytes, nstages);
-  const bool delta = delta_mode != 0;
+  constexpr uint32_t BMB = ELEMS / 8;
+  const Ring r = ring_setup(smem, a.stage_bytes, a.nstages);
+  const bool delta = a.delta_mode != 0;
+  const bool count = a.counters != nullptr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kCWarps) {
-    if (lane == 0) produce<ESZ, N>(plan, r, !delta, nullptr, 0);
+    if (lane == 0) produce<ESZ, N>(a.plan, r, !delta, (count && a.dropout_mode == 2) ? a.bitmap : nullptr,
+                                   a.words_per_row);
     return;
   }
   __shared__ double red[kCWarps][N];
   const int tid = threadIdx.x;
   uint32_t q = 0;
-  for (uint32_t item = blockIdx.x; item < plan.n_items; item += gridDim.x) {
-    const ItemGeom g = item_geom(plan, item);
-    double acc[N];
+  for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
+    const ItemGeom g = item_geom(a.plan, item);
+    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    double acc[N][2];
+    uint32_t nz[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) acc[i] = 0.0;
+    for (int i = 0; i < N; ++i) {
+      acc[i][0] = acc[i][1] = 0.0;
+      nz[i] = 0;
+    }
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_elems = ((n * ESZ) & ~15u) / ESZ;
       const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
       mbar_wait(&r.full[s], ph);
       const uint8_t* sb = r.buf + s * r.stage_bytes;
+      const uint8_t* bm = sb + (N + 1) * SB;
       const uint32_t nvec = main_elems / VEC;
       for (uint32_t v = tid; v < nvec; v += kCThreads) {
+        const uint32_t le = v * VEC;
         double b[VEC];
         if (!delta) VecIO<DT>::f64(lds128(sb + v * 16), b);
+        else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) b[e] = 0.0;
+        }
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           double x[VEC];
           VecIO<DT>::f64(lds128(sb + (i + (delta ? 0 : 1)) * SB + v * 16), x);
+          uint32_t keep = (1u << VEC) - 1u;
+          if (count && a.dropout_mode == 2) {
+            keep = (bm[i * BMB + (le >> 3)] >> (le & 7)) & ((1u << VEC) - 1u);
+          } else if (count && a.dropout_mode == 1) {
+            keep = 0;
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) keep |= (uint32_t)keep_draw(a.seed[i], jtensor0 + off + le + e, a.thresh) << e;
+          }
 #pragma unroll
           for (int e = 0; e < VEC; ++e) {
             const double d = delta ? x[e] : x[e] - b[e];
-            acc[i] = fma(d, d, acc[i]);
+            acc[i][e & 1] = fma(d, d, acc[i][e & 1]);
+            if (count) nz[i] += ((keep >> e) & 1u) && (d != 0.0);
           }
         }
       }
@@ -219,7 +253,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < N; ++i) {
           const double x = load_f64<DT>(g.seg->expert[i], idx);
           const double d = delta ? x : x - b;
-          acc[i] = fma(d, d, acc[i]);
+          acc[i][0] = fma(d, d, acc[i][0]);
+          if (count) {
+            const bool keep = a.dropout_mode == 0 || keep_draw(a.seed[i], jtensor0 + off + e, a.thresh);
+            nz[i] += keep && (d != 0.0);
+          }
         }
       }
       __syncwarp();
@@ -228,15 +266,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double w = warp_sum_f64(acc[i]);
+      const double w = warp_sum_f64(acc[i][0] + acc[i][1]);
       if (lane == 0) red[warp][i] = w;
+      if (count) {
+        const uint32_t z = __reduce_add_sync(0xffffffffu, nz[i]);
+        if (lane == 0 && z) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + i, (unsigned long long)z);
+      }
     }
     cbar_sync();
     if (tid < N) {
       double t = red[0][tid];
 #pragma unroll
       for (int w = 1; w < kCWarps; ++w) t += red[w][tid];
-      partials[(uint64_t)g.gitem * N + tid] = t;
+      a.partials[(uint64_t)g.gitem * N + tid] = t;
     }
     cbar_sync();
   }
@@ -462,9 +504,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
     ElemConsts c;
 #pragma unroll
     for (int i = 0; i < N; ++i) c.scale[i] = __ldg(scale + i);
-    uint32_t cnt_nz[N], cnt_er[N];
+    uint32_t cnt_er[N];  // entries erased (non-zero entries after dropout are counted by K1)
 #pragma unroll
-    for (int i = 0; i < N; ++i) cnt_nz[i] = cnt_er[i] = 0;
+    for (int i = 0; i < N; ++i) cnt_er[i] = 0;
     const uint64_t jtensor0 = g.seg->j0 + g.start;
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
@@ -497,10 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
             uint32_t nzm, erm;
             y[e] = merge_elem_f64<N>(b[e], X, keep, a, c, nzm, erm);
 #pragma unroll
-            for (int i = 0; i < N; ++i) {
-              cnt_nz[i] += (nzm >> i) & 1u;
-              cnt_er[i] += (erm >> i) & 1u;
-            }
+            for (int i = 0; i < N; ++i) cnt_er[i] += (erm >> i) & 1u;
           }
           store_vec_f64<DTO, VEC>(g.seg->out, out_base + le, y);
         }
@@ -521,10 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
         uint32_t nzm, erm;
         const double Y = merge_elem_f64<N>(B, X, keep, a, c, nzm, erm);
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          cnt_nz[i] += (nzm >> i) & 1u;
-          cnt_er[i] += (erm >> i) & 1u;
-        }
+        for (int i = 0; i < N; ++i) cnt_er[i] += (erm >> i) & 1u;
+        (void)nzm;
         store_from_f64<DTO>(g.seg->out, idx, Y);
       }
       __syncwarp();
@@ -534,12 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
     // per-item counters -> per-tensor u64 totals (integer atomics: order-independent)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const uint32_t z = __reduce_add_sync(0xffffffffu, cnt_nz[i]);
       const uint32_t er = __reduce_add_sync(0xffffffffu, cnt_er[i]);
-      if (lane == 0) {
-        if (z) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + i, (unsigned long long)z);
-        if (er) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + N + i, (unsigned long long)er);
-      }
+      if (lane == 0 && er) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + N + i, (unsigned long long)er);
     }
   }
 }
@@ -556,6 +589,24 @@ __device__ __forceinline__ uint32_t mask_lt0(float x) {  // 0xffffffff iff x < 0
   return r;
 }
 __device__ __forceinline__ float andnot_f(float x, uint32_t m) { return __uint_as_float(__float_as_uint(x) & ~m); }
+// c + (x >> 31) as one IMAD.HI on the FMA pipe: hi32(x * 2) + c
+__device__ __forceinline__ uint32_t add_sign_bit(uint32_t x, uint32_t c) {
+  uint32_t r;
+  asm("mad.hi.u32 %0, %1, 2, %2;" : "=r"(r) : "r"(x), "r"(c));
+  return r;
+}
+// +-1.0f with the sign of x (one LOP3)
+__device__ __forceinline__ float sign_one(float x) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(r) : "r"(__float_as_uint(x)), "r"(0x80000000u), "r"(0x3f800000u));
+  return __uint_as_float(r);
+}
+// the bf16 rounding midpoint of the interval containing y: (bits & 0xffff0000) | 0x8000 (one LOP3)
+__device__ __forceinline__ float mid_of(float y) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(r) : "r"(__float_as_uint(y)), "r"(0xffff0000u), "r"(0x8000u));
+  return __uint_as_float(r);
+}
 
 // Fast K3 for bf16 experts + bf16 base -> bf16 (the checkpoint path): f32x2 arithmetic with certified
 // guards; DROP 0 = no dropout, 2 = keep bits from the K2 bitmap; ERASE 0 off, 1 sum vote, 2 squared vote.
@@ -597,9 +648,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constan
       // k = d * sr cannot underflow for bf16 deltas (|d| >= 2^-133) when sr >= 2^-16
       fast_ok = fast_ok && sr32[i] >= 0x1p-16f && sr32[i] < 0x1p100f;
     }
-    uint32_t cnt_nz[N], cnt_er[N];  // counted negatively through all-ones masks
+    uint32_t cnt_er[N];  // entries erased (non-zero entries after dropout are counted by K1)
 #pragma unroll
-    for (int i = 0; i < N; ++i) cnt_nz[i] = cnt_er[i] = 0;
+    for (int i = 0; i < N; ++i) cnt_er[i] = 0;
     const uint64_t jtensor0 = g.seg->j0 + g.start;
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
@@ -639,11 +690,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constan
             } else {
               k2[i] = __fmul2_rn(d2, make_float2(sr32[i], sr32[i]));
             }
-            cnt_nz[i] -= mask_ne0(k2[i].x);
-            cnt_nz[i] -= mask_ne0(k2[i].y);
             aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
           }
           bool sl = false, sh = false;
+          float2 y2;
           if constexpr (kErase) {
             float2 vv, gg;
             if (ERASE == 1) {
@@ -660,29 +710,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constan
                 gg = __ffma2_rn(k2[i], k2[i], gg);
               }
             }
-            // |vote| must clear the certified error bound (an all-zero column is an exact tie)
-            sl = (gg.x > 0.f) && !(fabsf(vv.x) > cv * gg.x);
-            sh = (gg.y > 0.f) && !(fabsf(vv.y) > cv * gg.y);
-            const float2 sg = make_float2(copysignf(1.f, vv.x), copysignf(1.f, vv.y));
+            // |vote| must clear the certified error bound; an all-zero column (vote = bound = 0) is an
+            // exact tie and needs no fallback
+            const float2 cg = __fmul2_rn(make_float2(cv, cv), gg);
+            sl = !(fabsf(vv.x) >= cg.x);
+            sh = !(fabsf(vv.y) >= cg.y);
+            const float2 sg = make_float2(sign_one(vv.x), sign_one(vv.y));
+            // t = k * sign(vote) + 0 (exact; +0 for k = 0): t < 0 <=> entry opposes the majority.
+            // Erased entries are counted from t's sign bit on the FMA pipe, survivors kept as max(t, 0).
+            float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int i = 0; i < N; ++i) {
-              const float2 t2 = __fmul2_rn(k2[i], sg);
-              const uint32_t ml = mask_lt0(t2.x), mh = mask_lt0(t2.y);
-              cnt_er[i] -= ml;
-              cnt_er[i] -= mh;
-              k2[i] = make_float2(andnot_f(k2[i].x, ml), andnot_f(k2[i].y, mh));
+              const float2 t2 = __ffma2_rn(k2[i], sg, make_float2(0.f, 0.f));
+              cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i]);
+              cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i]);
+              acc = __ffma2_rn(make_float2(w32[i], w32[i]), make_float2(fmaxf(t2.x, 0.f), fmaxf(t2.y, 0.f)), acc);
             }
-          }
-          float2 y2 = b2;
+            y2 = __ffma2_rn(sg, acc, b2);
+          } else {
+            y2 = b2;
 #pragma unroll
-          for (int i = 0; i < N; ++i) y2 = __ffma2_rn(make_float2(w32[i], w32[i]), k2[i], y2);
+            for (int i = 0; i < N; ++i) y2 = __ffma2_rn(make_float2(w32[i], w32[i]), k2[i], y2);
+          }
           // bf16 rounding must be certain: distance to the rounding midpoint > error bound
           const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, make_float2(fabsf(b2.x), fabsf(b2.y)));
-          const float2 mid = make_float2(__uint_as_float((__float_as_uint(y2.x) & 0xffff0000u) | 0x8000u),
-                                         __uint_as_float((__float_as_uint(y2.y) & 0xffff0000u) | 0x8000u));
+          const float2 mid = make_float2(mid_of(y2.x), mid_of(y2.y));
           const float2 dm = __fadd2_rn(y2, make_float2(-mid.x, -mid.y));
-          sl = sl || !(fabsf(dm.x) > 0x1p-19f * S2.x);
-          sh = sh || !(fabsf(dm.y) > 0x1p-19f * S2.y);
+          const float2 eb = __fmul2_rn(make_float2(0x1p-19f, 0x1p-19f), S2);
+          sl = sl || !(fabsf(dm.x) > eb.x);
+          sh = sh || !(fabsf(dm.y) > eb.y);
           slowm |= ((uint32_t)sl | ((uint32_t)sh << 1)) << (2 * p);
           __nv_bfloat162 p2 = __floats2bfloat162_rn(y2.x, y2.y);
           outw[p] = *reinterpret_cast<uint32_t*>(&p2);
@@ -706,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constan
               if constexpr (kErase) {
                 const uint32_t fo = fast_opp_bits<N>(be, xe.v, keep, sr32, ERASE, false);
 #pragma unroll
-                for (int i = 0; i < N; ++i) cnt_er[i] -= ((fo >> i) & 1u) - ((erm >> i) & 1u);
+                for (int i = 0; i < N; ++i) cnt_er[i] += ((erm >> i) & 1u) - ((fo >> i) & 1u);
               }
               const uint32_t hb = f64_to_bf16_rne(Y);
               uint32_t& w = outw[e >> 1];
@@ -733,10 +789,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constan
         uint32_t nzm, erm;
         const double Y = merge_elem_f64<N>(B, X, keep, a, c, nzm, erm);
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          cnt_nz[i] -= 0u - ((nzm >> i) & 1u);
-          cnt_er[i] -= 0u - ((erm >> i) & 1u);
-        }
+        for (int i = 0; i < N; ++i) cnt_er[i] += (erm >> i) & 1u;
+        (void)nzm;
         store_from_f64<RLK_BF16>(g.seg->out, idx, Y);
       }
       __syncwarp();
@@ -745,12 +799,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constan
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const uint32_t z = __reduce_add_sync(0xffffffffu, cnt_nz[i]);
       const uint32_t er = __reduce_add_sync(0xffffffffu, cnt_er[i]);
-      if (lane == 0) {
-        if (z) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + i, (unsigned long long)z);
-        if (er) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + N + i, (unsigned long long)er);
-      }
+      if (lane == 0 && er) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + N + i, (unsigned long long)er);
     }
   }
 }
@@ -773,15 +823,18 @@ static int ensure_smem(K kernel, uint32_t bytes) {
 }
 
 template <int DT, int N>
-static int launch_sumsq(const rlk_fusion_plan& plan, int delta, double* partials, cudaStream_t s) {
+static int launch_sumsq(SumsqArgs& a, cudaStream_t s) {
   uint32_t sb, ns;
-  stage_geometry<N>(Elem<DT>::size, false, sb, ns);
+  stage_geometry<N>(Elem<DT>::size, a.counters && a.dropout_mode == 2, sb, ns);
+  ns = std::max<uint32_t>(2u, std::min<uint32_t>(ns / 2, 4u));  // two CTAs per SM
+  a.stage_bytes = sb;
+  a.nstages = ns;
   const uint32_t smem = 1024 + sb * ns;
   auto kern = k_sumsq<DT, N>;
   int st = ensure_smem(kern, smem);
   if (st) return st;
-  uint32_t grid = std::min<uint32_t>(plan.n_items, (uint32_t)sm_count());
-  kern<<<grid, kThreads, smem, s>>>(plan, delta, partials, sb, ns);
+  uint32_t grid = std::min<uint32_t>(a.plan.n_items, 2u * (uint32_t)sm_count());
+  kern<<<grid, kThreads, smem, s>>>(a);
   return launch_status("rlk_fusion_sumsq");
 }
 
@@ -828,16 +881,16 @@ static int launch_merge(MergeArgs& a, cudaStream_t s) {
 }
 
 template <int DT>
-static int dispatch_sumsq_n(int n, const rlk_fusion_plan& plan, int delta, double* partials, cudaStream_t s) {
+static int dispatch_sumsq_n(int n, SumsqArgs& a, cudaStream_t s) {
   switch (n) {
-    case 1: return launch_sumsq<DT, 1>(plan, delta, partials, s);
-    case 2: return launch_sumsq<DT, 2>(plan, delta, partials, s);
-    case 3: return launch_sumsq<DT, 3>(plan, delta, partials, s);
-    case 4: return launch_sumsq<DT, 4>(plan, delta, partials, s);
-    case 5: return launch_sumsq<DT, 5>(plan, delta, partials, s);
-    case 6: return launch_sumsq<DT, 6>(plan, delta, partials, s);
-    case 7: return launch_sumsq<DT, 7>(plan, delta, partials, s);
-    case 8: return launch_sumsq<DT, 8>(plan, delta, partials, s);
+    case 1: return launch_sumsq<DT, 1>(a, s);
+    case 2: return launch_sumsq<DT, 2>(a, s);
+    case 3: return launch_sumsq<DT, 3>(a, s);
+    case 4: return launch_sumsq<DT, 4>(a, s);
+    case 5: return launch_sumsq<DT, 5>(a, s);
+    case 6: return launch_sumsq<DT, 6>(a, s);
+    case 7: return launch_sumsq<DT, 7>(a, s);
+    case 8: return launch_sumsq<DT, 8>(a, s);
   }
   set_error("expert count %d not supported (1..%d)", n, RLK_MAX_EXPERTS);
   return RLK_ERR_UNSUPPORTED;
@@ -877,16 +930,32 @@ using namespace rlk;
 extern "C" {
 
 int rlk_fusion_sumsq(const rlk_fusion_plan* plan, int n_experts, int dtype, int delta_mode, double* partials,
-                     void* stream) {
+                     unsigned long long* nz_counters, int dropout_mode, const uint64_t* child_seeds, uint64_t thresh,
+                     const uint32_t* bitmap, uint64_t words_per_row, void* stream) {
   RLK_REQUIRE(plan != nullptr && partials != nullptr, "rlk_fusion_sumsq: NULL argument");
   RLK_REQUIRE(n_experts >= 1 && n_experts <= RLK_MAX_EXPERTS, "rlk_fusion_sumsq: bad expert count %d", n_experts);
+  RLK_REQUIRE(dropout_mode >= 0 && dropout_mode <= 2, "rlk_fusion_sumsq: bad dropout mode %d", dropout_mode);
+  RLK_REQUIRE(!nz_counters || dropout_mode == 0 || child_seeds, "rlk_fusion_sumsq: dropout needs child seeds");
+  RLK_REQUIRE(!nz_counters || dropout_mode != 2 || (bitmap && words_per_row % 4 == 0),
+              "rlk_fusion_sumsq: bitmap mode needs a bitmap with 16-byte rows");
   if (plan->n_items == 0) return RLK_OK;
   RLK_REQUIRE(plan->segs && plan->seg_item_prefix && plan->n_segs > 0, "rlk_fusion_sumsq: empty plan");
+  SumsqArgs a;
+  memset(&a, 0, sizeof(a));
+  a.plan = *plan;
+  a.partials = partials;
+  a.counters = nz_counters;
+  a.bitmap = bitmap;
+  a.words_per_row = words_per_row;
+  for (int i = 0; i < n_experts; ++i) a.seed[i] = child_seeds ? child_seeds[i] : 0;
+  a.thresh = thresh;
+  a.delta_mode = delta_mode;
+  a.dropout_mode = nz_counters ? dropout_mode : 0;
   cudaStream_t s = (cudaStream_t)stream;
   switch (dtype) {
-    case RLK_BF16: return dispatch_sumsq_n<RLK_BF16>(n_experts, *plan, delta_mode, partials, s);
-    case RLK_F32: return dispatch_sumsq_n<RLK_F32>(n_experts, *plan, delta_mode, partials, s);
-    case RLK_F64: return dispatch_sumsq_n<RLK_F64>(n_experts, *plan, delta_mode, partials, s);
+    case RLK_BF16: return dispatch_sumsq_n<RLK_BF16>(n_experts, a, s);
+    case RLK_F32: return dispatch_sumsq_n<RLK_F32>(n_experts, a, s);
+    case RLK_F64: return dispatch_sumsq_n<RLK_F64>(n_experts, a, s);
   }
   set_error("rlk_fusion_sumsq: bad dtype %d", dtype);
   return RLK_ERR_INVALID;

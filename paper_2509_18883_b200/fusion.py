@@ -240,11 +240,24 @@ class FusionCall:
         self.timers.setdefault(name, []).append((e0, e1))
 
     def run(self, weights: Sequence[float], dtype_out: torch.dtype | None = None) -> "FusionCall":
-        """One complete fusion step on the call's stream: zero counters, K1, [all_reduce], finalize,
-        [K2], K3.  Reusing a FusionCall across steps reuses its launch plan (host metadata only)."""
+        """One complete fusion step on the call's stream: zero counters, [K2], K1, [all_reduce],
+        finalize, K3.  Reusing a FusionCall across steps reuses its launch plan (host metadata only)."""
         with torch.cuda.stream(self.stream):
             self.counters.zero_()
         return self.norms().merge(weights, dtype_out)
+
+    def _bitmap(self, s) -> None:
+        """K2: keep bits for every (expert, within-tensor index < max extent) -- before K1, which
+        counts the non-zero entries after dropout, and K3."""
+        if self.dropout_mode != 2:
+            return
+        n_bits = ((self.plan.max_extent + 8191) // 8192) * 8192
+        self.words_per_row = n_bits // 32
+        if self.bitmap is None or self.bitmap.numel() != self.n * self.words_per_row:
+            self.bitmap = torch.empty(self.n * self.words_per_row, dtype=torch.int32, device=self.device)
+        seeds = (L.C.c_uint64 * self.n)(*self.seeds)
+        self._launch("rlk_fusion_mask_bitmap", seeds, self.n, self.thresh, n_bits, L.ptr(self.bitmap),
+                     self.words_per_row, s)
 
     # -- K1 + all_reduce + finalize
     def norms(self, precomputed_sumsq: torch.Tensor | None = None) -> "FusionCall":
@@ -259,8 +272,11 @@ class FusionCall:
                     self.partials = torch.zeros(self.layout.n_items * self.n, dtype=torch.float64, device=self.device)
                 elif world > 1:
                     self.partials.zero_()  # other ranks' slots must be exactly zero for the exact sum
+                self._bitmap(s)
+                seeds = (L.C.c_uint64 * self.n)(*self.seeds)
                 self._launch("rlk_fusion_sumsq", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
-                             int(self.delta_mode), L.ptr(self.partials), s)
+                             int(self.delta_mode), L.ptr(self.partials), L.ptr(self.counters), self.dropout_mode,
+                             seeds, self.thresh, L.ptr(self.bitmap), self.words_per_row, s)
                 if world > 1:
                     import torch.distributed as dist
                     # disjoint slots: the sum is exact, so norms are identical at every world size
@@ -290,14 +306,8 @@ class FusionCall:
         if self.n < 2:
             erase = 0
         with torch.cuda.stream(self.stream):
-            if self.dropout_mode == 2:
-                n_bits = ((self.plan.max_extent + 8191) // 8192) * 8192
-                self.words_per_row = n_bits // 32
-                if self.bitmap is None or self.bitmap.numel() != self.n * self.words_per_row:
-                    self.bitmap = torch.empty(self.n * self.words_per_row, dtype=torch.int32, device=self.device)
-                seeds = (L.C.c_uint64 * self.n)(*self.seeds)
-                self._launch("rlk_fusion_mask_bitmap", seeds, self.n, self.thresh, n_bits, L.ptr(self.bitmap),
-                             self.words_per_row, s)
+            if self.dropout_mode == 2 and self.bitmap is None:
+                self._bitmap(s)  # K3 without a preceding K1 (staged transforms)
             w = (L.C.c_double * self.n)(*[float(x) for x in weights])
             seeds = (L.C.c_uint64 * self.n)(*self.seeds)
             dmode = (1 | (2 if self.with_base else 0)) if self.delta_mode else 0

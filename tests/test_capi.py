@@ -40,6 +40,6 @@ def test_invalid_arguments_map_to_value_error():
     from paper_2509_18883_b200 import _lib as L
     L.lib()
     with pytest.raises(ValueError, match="expert count"):
-        L.call("rlk_fusion_sumsq", ctypes.byref(L.FusionPlanC(0, 0, 0, 1)), 9, 0, 0, 8, None)
+        L.call("rlk_fusion_sumsq", ctypes.byref(L.FusionPlanC(0, 0, 0, 1)), 9, 0, 0, 8, None, 0, None, 0, None, 0, None)
     with pytest.raises(ValueError, match="bad dtype"):
         L.call("rlk_nonfinite_count", 8, 7, 1, 8, None)

@@ -232,10 +232,15 @@ def test_sharded_items_identical(cuda):
             c = F.FusionCall(pieces, layout, 3, cfg)
             c.partials = partials
             from paper_2509_18883_b200 import _lib as L
-            L.call("rlk_fusion_sumsq", L.C.byref(c.plan.c), 3, L.RLK_BF16, 0, L.ptr(partials), L.stream_handle())
+            c._bitmap(L.stream_handle())
+            L.call("rlk_fusion_sumsq", L.C.byref(c.plan.c), 3, L.RLK_BF16, 0, L.ptr(partials), L.ptr(c.counters),
+                   c.dropout_mode, (L.C.c_uint64 * 3)(*c.seeds), c.thresh, L.ptr(c.bitmap), c.words_per_row,
+                   L.stream_handle())
             calls.append(c)
         counters = torch.zeros((3, 6), dtype=torch.int64, device=cuda)
         for c in calls:
+            counters += c.counters  # K1's non-zero counts
+            c.counters.zero_()
             L.call("rlk_fusion_finalize", L.ptr(partials), L.ptr(layout.tensor_items_device(cuda)), 3, 3, 1, 0.0,
                    L.ptr(c.sumsq), L.ptr(c.scale), L.ptr(c.status), L.stream_handle())
             c.merge(w)
