@@ -612,15 +612,15 @@ __device__ __forceinline__ float mid_of(float y) {
 // guards; DROP 0 = no dropout, 2 = keep bits from the K2 bitmap; ERASE 0 off, 1 sum vote, 2 squared vote.
 // Elements whose guard trips are recomputed exactly (merge_elem_slow) in a rarely-taken phase 2.
 template <int N, int DROP, int ERASE>
-__global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constant__ MergeArgs a) {
+__global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_constant__ MergeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t SB = StreamBytes<N>::v;
   constexpr uint32_t ELEMS = SB / 2;
   constexpr uint32_t BMB = ELEMS / 8;
   constexpr bool kErase = (ERASE != 0) && (N >= 2);
-  const Ring r = ring_setup(smem, a.stage_bytes, a.nstages);
+  const Ring r = ring_setup(smem, a.stage_bytes, a.nstages, kFastCWarps);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == kCWarps) {
+  if (warp == kFastCWarps) {
     if (lane == 0) produce<2, N>(a.plan, r, true, DROP == 2 ? a.bitmap : nullptr, a.words_per_row);
     return;
   }
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constan
       const uint8_t* bm = sb + (N + 1) * SB;
       const uint32_t nvec = main_elems / 8;
       const uint64_t out_base = g.start + off;
-      for (uint32_t v = fast_ok ? tid : nvec; v < nvec; v += kCThreads) {
+      for (uint32_t v = fast_ok ? tid : nvec; v < nvec; v += kFastCThreads) {
         const uint32_t le = v * 8;
         const uint4 bw4 = lds128(sb + v * 16);
         uint4 xw4[N];
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge_fast(const __grid_constan
       }
       // items the fast path cannot certify, and the < 16-byte tail: exact f64 path
       const uint32_t e0 = fast_ok ? main_elems : 0;
-      for (uint32_t e = e0 + tid; e < n; e += kCThreads) {
+      for (uint32_t e = e0 + tid; e < n; e += kFastCThreads) {
         const uint64_t idx = g.start + off + e;
         const double B = load_f64<RLK_BF16>(g.seg->base, idx);
         double X[N];
@@ -845,7 +845,7 @@ static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
   int st = ensure_smem(kern, smem);
   if (st) return st;
   uint32_t grid = std::min<uint32_t>(a.plan.n_items, (uint32_t)sm_count());
-  kern<<<grid, kThreads, smem, s>>>(a);
+  kern<<<grid, kFastThreads, smem, s>>>(a);
   return launch_status("rlk_fusion_merge");
 }
 

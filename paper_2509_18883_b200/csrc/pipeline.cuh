@@ -12,6 +12,11 @@ constexpr int kThreads = kCThreads + 32;
 
 __device__ __forceinline__ void cbar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory"); }
 
+// K3 fast path consumer warps (8: more forces <= 128 registers and spills)
+constexpr int kFastCWarps = 8;
+constexpr int kFastCThreads = kFastCWarps * 32;
+constexpr int kFastThreads = kFastCThreads + 32;
+
 struct Ring {
   uint8_t* buf;
   uint64_t* full;
@@ -20,7 +25,8 @@ struct Ring {
   uint32_t nstages;
 };
 
-__device__ __forceinline__ Ring ring_setup(uint8_t* smem, uint32_t stage_bytes, uint32_t nstages) {
+__device__ __forceinline__ Ring ring_setup(uint8_t* smem, uint32_t stage_bytes, uint32_t nstages,
+                                           uint32_t consumer_warps = kCWarps) {
   Ring r;
   r.full = reinterpret_cast<uint64_t*>(smem);
   r.empty = r.full + nstages;
@@ -30,7 +36,7 @@ __device__ __forceinline__ Ring ring_setup(uint8_t* smem, uint32_t stage_bytes, 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < nstages; ++s) {
       mbar_init(&r.full[s], 1);
-      mbar_init(&r.empty[s], kCWarps);
+      mbar_init(&r.empty[s], consumer_warps);
     }
     fence_mbar_init();
   }
