@@ -162,6 +162,25 @@ int rlk_scaled_add(const void* a, const void* b, double alpha, void* out, int dt
 int rlk_synth_normal(void* out, int dtype, uint64_t n, uint64_t j0, uint64_t seed, double std_dev,
                      const void* base, void* stream);
 
+/* ---- K7 host streaming loader (checkpoints larger than HBM) -------------------------------------
+ * A ring of n_slots pinned host slots of slot_bytes each and n_threads host workers (0 = all cores).
+ * h2d / d2h pipeline pageable<->pinned memcpy against cudaMemcpyAsync on `stream`; the device side of
+ * a copy is complete when `stream` reaches the point of the call.  Loader state is not thread-safe:
+ * one loader per host thread.  Replaces: no reference counterpart (the reference holds everything in
+ * RAM as float64); the on-disk format it feeds is SPEC.md:588/727 (see loader.py). */
+void* rlk_loader_create(uint64_t slot_bytes, int n_slots, int n_threads);
+void rlk_loader_destroy(void* loader);
+const char* rlk_loader_last_error(void);
+int rlk_loader_h2d(void* loader, void* dst_dev, const void* src_host, uint64_t bytes, void* stream);
+int rlk_loader_d2h(void* loader, void* dst_host, const void* src_dev, uint64_t bytes, void* stream);
+/* Synthesise random-init parameters [j0, j0+n) into pinned slots on the host workers and DMA them:
+ * value(j) = RN(base(j) + noise_std * N(noise_seed, j)), base(j) = RN(base_std * N(base_seed, j)),
+ * noise_seed 0 = the base itself.  dtype RLK_BF16 or RLK_F32. */
+int rlk_loader_synth_h2d(void* loader, void* dst_dev, int dtype, uint64_t n, uint64_t j0, uint64_t base_seed,
+                         double base_std, uint64_t noise_seed, double noise_std, void* stream);
+/* D2H through the slots, folding the data into *checksum (sum of 64-bit words mod 2^64); bytes % 8 == 0. */
+int rlk_loader_d2h_checksum(void* loader, const void* src_dev, uint64_t bytes, uint64_t* checksum, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

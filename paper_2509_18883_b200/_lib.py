@@ -63,12 +63,13 @@ SIGNATURES = {
     "rlk_nonfinite_count": (_I, [_P, _I, _U64, _P, _P]),
     "rlk_scaled_add": (_I, [_P, _P, _D, _P, _I, _U64, _P]),
     "rlk_synth_normal": (_I, [_P, _I, _U64, _U64, _U64, _D, _P, _P]),
-    "rlk_loader_create": (_P, [_U64, _I]),
+    "rlk_loader_create": (_P, [_U64, _I, _I]),
     "rlk_loader_destroy": (None, [_P]),
-    "rlk_loader_stage": (_I, [_P, _P, _P, _U64, _P]),
-    "rlk_loader_buffer": (_P, [_P, _I]),
-    "rlk_loader_sync_slot": (_I, [_P, _I]),
-    "rlk_loader_copy_out": (_I, [_P, _P, _U64, _P]),
+    "rlk_loader_last_error": (C.c_char_p, []),
+    "rlk_loader_h2d": (_I, [_P, _P, _P, _U64, _P]),
+    "rlk_loader_d2h": (_I, [_P, _P, _P, _U64, _P]),
+    "rlk_loader_synth_h2d": (_I, [_P, _P, _I, _U64, _U64, _U64, _D, _U64, _D, _P]),
+    "rlk_loader_d2h_checksum": (_I, [_P, _P, _U64, C.POINTER(C.c_uint64), _P]),
 }
 
 _lib = None

@@ -1,0 +1,327 @@
+// K7: host streaming loader for checkpoints larger than HBM.
+//
+// A ring of pinned host slots and a pool of worker threads.  Host -> device: each slot-sized chunk is
+// copied (or synthesised) into a free pinned slot by all workers in parallel, then DMA'd with
+// cudaMemcpyAsync on the caller's stream; an event per slot tells when the slot may be reused, so the
+// memcpy of chunk k+1 overlaps the DMA of chunk k.  Device -> host runs the mirror image.  One
+// cudaMemcpyAsync per chunk (no batched-copy APIs).
+//
+// Synthesis mode reproduces the benchmark's random-init experts without a host copy of the
+// checkpoint: value(j) = RN_dtype(base(j) + std_e * N(seed_e, j)) with base(j) = RN_dtype(std_b * N(seed_b, j)),
+// N(seed, j) a Box-Muller normal of the SplitMix64 hash mix64(seed ^ mix64(j + 1)).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "../../include/rlk.h"
+
+namespace {
+
+thread_local char g_err[256] = "";
+
+int fail(const char* what, cudaError_t e) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+  return RLK_ERR_CUDA;
+}
+
+inline uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+inline float normal_of(uint64_t seed, uint64_t j) {
+  const uint64_t h = mix64(seed ^ mix64(j + 1));
+  const float u1 = ((uint32_t)(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
+  const float u2 = (uint32_t)(h & 0xffffffu) * (1.0f / 16777216.0f);
+  return std::sqrt(-2.0f * std::log(u1)) * std::cos(6.283185307f * u2);
+}
+
+inline uint16_t f32_to_bf16(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+inline float bf16_to_f32(uint16_t h) {
+  uint32_t u = (uint32_t)h << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+class Pool {
+ public:
+  explicit Pool(int n) {
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  int size() const { return (int)workers_.size(); }
+  // run f(worker_index) on every worker, wait for all
+  void run(const std::function<void(int)>& f) {
+    std::unique_lock<std::mutex> lk(m_);
+    job_ = &f;
+    pending_ = (int)workers_.size();
+    ++gen_;
+    cv_.notify_all();
+    done_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int idx) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        job = job_;
+      }
+      (*job)(idx);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+struct Loader {
+  uint64_t slot_bytes;
+  std::vector<void*> slots;
+  std::vector<cudaEvent_t> events;
+  std::vector<bool> armed;
+  Pool pool;
+  int next = 0;
+  Loader(uint64_t sb, int n, int threads) : slot_bytes(sb), pool(threads) {}
+};
+
+int acquire(Loader* L, int& slot) {
+  slot = L->next;
+  L->next = (L->next + 1) % (int)L->slots.size();
+  if (L->armed[slot]) {
+    cudaError_t e = cudaEventSynchronize(L->events[slot]);
+    if (e != cudaSuccess) return fail("rlk_loader: event sync", e);
+    L->armed[slot] = false;
+  }
+  return RLK_OK;
+}
+
+void parallel_copy(Loader* L, void* dst, const void* src, uint64_t n) {
+  const int T = L->pool.size();
+  if (n < (1u << 20) || T == 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  L->pool.run([&](int w) {
+    const uint64_t per = ((n + T - 1) / T + 63) & ~63ull;
+    const uint64_t a = std::min<uint64_t>(n, per * w), b = std::min<uint64_t>(n, a + per);
+    if (b > a) std::memcpy((char*)dst + a, (const char*)src + a, b - a);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+void* rlk_loader_create(uint64_t slot_bytes, int n_slots, int n_threads) {
+  if (slot_bytes == 0 || n_slots < 2) return nullptr;
+  if (n_threads <= 0) n_threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  auto* L = new Loader(slot_bytes, n_slots, n_threads);
+  for (int i = 0; i < n_slots; ++i) {
+    void* p = nullptr;
+    cudaEvent_t ev;
+    if (cudaHostAlloc(&p, slot_bytes, cudaHostAllocDefault) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+      for (void* q : L->slots) cudaFreeHost(q);
+      delete L;
+      return nullptr;
+    }
+    L->slots.push_back(p);
+    L->events.push_back(ev);
+    L->armed.push_back(false);
+  }
+  return L;
+}
+
+void rlk_loader_destroy(void* ld) {
+  auto* L = (Loader*)ld;
+  if (!L) return;
+  for (size_t i = 0; i < L->slots.size(); ++i) {
+    if (L->armed[i]) cudaEventSynchronize(L->events[i]);
+    cudaEventDestroy(L->events[i]);
+    cudaFreeHost(L->slots[i]);
+  }
+  delete L;
+}
+
+const char* rlk_loader_last_error(void) { return g_err; }
+
+int rlk_loader_h2d(void* ld, void* dst_dev, const void* src_host, uint64_t bytes, void* stream) {
+  auto* L = (Loader*)ld;
+  if (!L || (!dst_dev && bytes) || (!src_host && bytes)) return RLK_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (uint64_t off = 0; off < bytes; off += L->slot_bytes) {
+    const uint64_t n = std::min<uint64_t>(L->slot_bytes, bytes - off);
+    int slot;
+    if (int st = acquire(L, slot)) return st;
+    parallel_copy(L, L->slots[slot], (const char*)src_host + off, n);
+    cudaError_t e = cudaMemcpyAsync((char*)dst_dev + off, L->slots[slot], n, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return fail("rlk_loader_h2d: cudaMemcpyAsync", e);
+    if ((e = cudaEventRecord(L->events[slot], s)) != cudaSuccess) return fail("rlk_loader_h2d: event", e);
+    L->armed[slot] = true;
+  }
+  return RLK_OK;
+}
+
+int rlk_loader_d2h(void* ld, void* dst_host, const void* src_dev, uint64_t bytes, void* stream) {
+  auto* L = (Loader*)ld;
+  if (!L || (bytes && (!dst_host || !src_dev))) return RLK_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  // issue all DMAs for a window of slots first, then drain them in order (copy-out overlaps DMA)
+  const int ns = (int)L->slots.size();
+  std::vector<std::pair<int, uint64_t>> inflight;
+  auto drain_one = [&]() -> int {
+    auto [slot, off] = inflight.front();
+    inflight.erase(inflight.begin());
+    cudaError_t e = cudaEventSynchronize(L->events[slot]);
+    if (e != cudaSuccess) return fail("rlk_loader_d2h: event sync", e);
+    L->armed[slot] = false;
+    const uint64_t n = std::min<uint64_t>(L->slot_bytes, bytes - off);
+    parallel_copy(L, (char*)dst_host + off, L->slots[slot], n);
+    return RLK_OK;
+  };
+  for (uint64_t off = 0; off < bytes; off += L->slot_bytes) {
+    if ((int)inflight.size() == ns - 1)
+      if (int st = drain_one()) return st;
+    const uint64_t n = std::min<uint64_t>(L->slot_bytes, bytes - off);
+    int slot;
+    if (int st = acquire(L, slot)) return st;
+    cudaError_t e = cudaMemcpyAsync(L->slots[slot], (const char*)src_dev + off, n, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return fail("rlk_loader_d2h: cudaMemcpyAsync", e);
+    if ((e = cudaEventRecord(L->events[slot], s)) != cudaSuccess) return fail("rlk_loader_d2h: event", e);
+    L->armed[slot] = true;
+    inflight.emplace_back(slot, off);
+  }
+  while (!inflight.empty())
+    if (int st = drain_one()) return st;
+  return RLK_OK;
+}
+
+// Synthesise n elements [j0, j0+n) of a random-init tensor straight into pinned slots and DMA them.
+// dtype RLK_BF16 or RLK_F32.  noise_seed == 0 -> the base tensor itself.
+int rlk_loader_synth_h2d(void* ld, void* dst_dev, int dtype, uint64_t n, uint64_t j0, uint64_t base_seed,
+                         double base_std, uint64_t noise_seed, double noise_std, void* stream) {
+  auto* L = (Loader*)ld;
+  if (!L || (n && !dst_dev) || (dtype != RLK_BF16 && dtype != RLK_F32)) return RLK_ERR_INVALID;
+  const uint64_t esz = dtype == RLK_BF16 ? 2 : 4;
+  const uint64_t per_slot = L->slot_bytes / esz;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int T = L->pool.size();
+  for (uint64_t e0 = 0; e0 < n; e0 += per_slot) {
+    const uint64_t m = std::min<uint64_t>(per_slot, n - e0);
+    int slot;
+    if (int st = acquire(L, slot)) return st;
+    void* buf = L->slots[slot];
+    L->pool.run([&](int w) {
+      const uint64_t per = (m + T - 1) / T;
+      const uint64_t a = std::min<uint64_t>(m, per * w), b = std::min<uint64_t>(m, a + per);
+      for (uint64_t i = a; i < b; ++i) {
+        const uint64_t j = j0 + e0 + i;
+        float base = (float)base_std * normal_of(base_seed, j);
+        if (dtype == RLK_BF16) {
+          base = bf16_to_f32(f32_to_bf16(base));
+          const float v = noise_seed ? base + (float)noise_std * normal_of(noise_seed, j) : base;
+          ((uint16_t*)buf)[i] = f32_to_bf16(v);
+        } else {
+          const float v = noise_seed ? base + (float)noise_std * normal_of(noise_seed, j) : base;
+          ((float*)buf)[i] = v;
+        }
+      }
+    });
+    cudaError_t e = cudaMemcpyAsync((char*)dst_dev + e0 * esz, buf, m * esz, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return fail("rlk_loader_synth_h2d: cudaMemcpyAsync", e);
+    if ((e = cudaEventRecord(L->events[slot], s)) != cudaSuccess) return fail("rlk_loader_synth_h2d: event", e);
+    L->armed[slot] = true;
+  }
+  return RLK_OK;
+}
+
+// D2H into pinned slots and fold every 64-bit word into a checksum (a sink for outputs too large to
+// keep on the host): *checksum += sum of words (mod 2^64), order-independent.
+int rlk_loader_d2h_checksum(void* ld, const void* src_dev, uint64_t bytes, uint64_t* checksum, void* stream) {
+  auto* L = (Loader*)ld;
+  if (!L || !checksum || (bytes && !src_dev) || (bytes & 7)) return RLK_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::atomic<uint64_t> acc{0};
+  const int T = L->pool.size();
+  const int ns = (int)L->slots.size();
+  std::vector<std::pair<int, uint64_t>> inflight;
+  auto drain_one = [&]() -> int {
+    auto [slot, off] = inflight.front();
+    inflight.erase(inflight.begin());
+    cudaError_t e = cudaEventSynchronize(L->events[slot]);
+    if (e != cudaSuccess) return fail("rlk_loader_d2h_checksum: event sync", e);
+    L->armed[slot] = false;
+    const uint64_t words = std::min<uint64_t>(L->slot_bytes, bytes - off) / 8;
+    const uint64_t* w64 = (const uint64_t*)L->slots[slot];
+    L->pool.run([&](int w) {
+      const uint64_t per = (words + T - 1) / T;
+      const uint64_t a = std::min<uint64_t>(words, per * w), b = std::min<uint64_t>(words, a + per);
+      uint64_t local = 0;
+      for (uint64_t i = a; i < b; ++i) local += w64[i];
+      acc.fetch_add(local, std::memory_order_relaxed);
+    });
+    return RLK_OK;
+  };
+  for (uint64_t off = 0; off < bytes; off += L->slot_bytes) {
+    if ((int)inflight.size() == ns - 1)
+      if (int st = drain_one()) return st;
+    const uint64_t n = std::min<uint64_t>(L->slot_bytes, bytes - off);
+    int slot;
+    if (int st = acquire(L, slot)) return st;
+    cudaError_t e = cudaMemcpyAsync(L->slots[slot], (const char*)src_dev + off, n, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return fail("rlk_loader_d2h_checksum: cudaMemcpyAsync", e);
+    if ((e = cudaEventRecord(L->events[slot], s)) != cudaSuccess) return fail("rlk_loader_d2h_checksum: event", e);
+    L->armed[slot] = true;
+    inflight.emplace_back(slot, off);
+  }
+  while (!inflight.empty())
+    if (int st = drain_one()) return st;
+  *checksum += acc.load();
+  return RLK_OK;
+}
+
+}  // extern "C"

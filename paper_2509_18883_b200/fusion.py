@@ -278,9 +278,9 @@ class FusionCall:
                              int(self.delta_mode), L.ptr(self.partials), L.ptr(self.counters), self.dropout_mode,
                              seeds, self.thresh, L.ptr(self.bitmap), self.words_per_row, s)
                 if world > 1:
-                    import torch.distributed as dist
                     # disjoint slots: the sum is exact, so norms are identical at every world size
-                    dist.all_reduce(self.partials, op=dist.ReduceOp.SUM, group=self.group)
+                    from .dist import allreduce_partials
+                    allreduce_partials(self.partials, self.group)
                 self._launch("rlk_fusion_finalize", L.ptr(self.partials),
                        L.ptr(self.layout.tensor_items_device(self.device)), self.layout.n_tensors, self.n,
                        self.cfg.target_mode, float(self.cfg.target_norm) if self.cfg.target_mode == 2 else 0.0,

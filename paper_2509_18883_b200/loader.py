@@ -1,0 +1,218 @@
+"""Streaming fusion of checkpoints larger than HBM (BASELINE configs[3]).
+
+Host state dicts (numpy arrays, CPU torch tensors, memory maps) are fused tensor-group by tensor-group:
+each group's base + N experts are copied host -> device through the C++ loader (`rlk_loader_*`:
+pinned slot ring + worker threads, csrc/loader.cpp) on a copy stream, fused on a compute stream
+(K2 -> K1 -> finalize -> K3, exactly `fuse_state_dict` on the group), and the fused group is copied
+back device -> host while the next group streams in.  Device workspaces are double-buffered, so
+H2D of group g+1 overlaps the kernels and the D2H of group g.
+
+Per-tensor semantics are those of the reference `fuse` (fusion.py:154-188) with one shared cfg; a
+tensor must fit in half the device budget (large MoE checkpoints store experts per matrix).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Mapping, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .fusion import FusionCall, FusionConfig, FusionLayout, FusionStats, Piece
+
+
+class HostLoader:
+    """RAII wrapper over the C++ pinned-slot loader."""
+
+    def __init__(self, slot_bytes: int = 64 << 20, n_slots: int = 4, n_threads: int = 0):
+        self._h = L.lib().rlk_loader_create(slot_bytes, n_slots, n_threads)
+        if not self._h:
+            raise L.RlkError("rlk_loader_create failed (pinned allocation)")
+
+    def _check(self, st: int, what: str) -> None:
+        if st != 0:
+            raise L.RlkError(f"{what}: {L.lib().rlk_loader_last_error().decode()} (status {st})")
+
+    def h2d(self, dst: torch.Tensor, src, stream) -> None:
+        arr = src if isinstance(src, np.ndarray) else src.numpy()
+        arr = np.ascontiguousarray(arr)
+        nbytes = dst.numel() * dst.element_size()
+        if arr.nbytes != nbytes:
+            raise ValueError(f"host/device size mismatch {arr.nbytes} != {nbytes}")
+        self._check(L.lib().rlk_loader_h2d(self._h, dst.data_ptr(), arr.ctypes.data, nbytes,
+                                           L.stream_handle(stream)), "rlk_loader_h2d")
+
+    def d2h(self, dst, src: torch.Tensor, stream) -> None:
+        arr = dst if isinstance(dst, np.ndarray) else dst.numpy()
+        nbytes = src.numel() * src.element_size()
+        if arr.nbytes != nbytes or not arr.flags.c_contiguous:
+            raise ValueError("host output must be a contiguous buffer of the device tensor's size")
+        self._check(L.lib().rlk_loader_d2h(self._h, arr.ctypes.data, src.data_ptr(), nbytes,
+                                           L.stream_handle(stream)), "rlk_loader_d2h")
+
+    def synth_h2d(self, dst: torch.Tensor, j0: int, base_seed: int, base_std: float, noise_seed: int,
+                  noise_std: float, stream) -> None:
+        self._check(L.lib().rlk_loader_synth_h2d(self._h, dst.data_ptr(), L.dtype_code(dst.dtype), dst.numel(), j0,
+                                                 base_seed, base_std, noise_seed, noise_std,
+                                                 L.stream_handle(stream)), "rlk_loader_synth_h2d")
+
+    def d2h_checksum(self, src: torch.Tensor, stream) -> int:
+        c = C.c_uint64(0)
+        self._check(L.lib().rlk_loader_d2h_checksum(self._h, src.data_ptr(), src.numel() * src.element_size(),
+                                                    C.byref(c), L.stream_handle(stream)), "rlk_loader_d2h_checksum")
+        return c.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            L.lib().rlk_loader_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+# ----------------------------------------------------------------------------- sources / sinks
+class ArraySource:
+    """Host arrays: base[name] and experts[i][name] (bf16 as torch CPU tensors or uint16 numpy)."""
+
+    def __init__(self, base: Mapping, experts: Sequence[Mapping]):
+        self.base, self.experts = base, experts
+
+    def fill(self, loader: HostLoader, name: str, stream_idx: int, dst: torch.Tensor, stream) -> None:
+        src = self.base[name] if stream_idx == 0 else self.experts[stream_idx - 1][name]
+        if isinstance(src, torch.Tensor):
+            src = src.contiguous().view(torch.int16).numpy() if src.dtype == torch.bfloat16 else src.numpy()
+        loader.h2d(dst, np.ascontiguousarray(src).reshape(-1), stream)
+
+
+class SyntheticSource:
+    """Random-init parameters synthesised on the host workers (counter hash; see loader.cpp)."""
+
+    def __init__(self, seed: int = 0, base_std: float = 0.02, expert_std: float = 1e-3):
+        self.seed, self.base_std, self.expert_std = seed, base_std, expert_std
+
+    def fill(self, loader: HostLoader, name: str, stream_idx: int, dst: torch.Tensor, stream) -> None:
+        from .core import mix64, label_hash
+        t = label_hash(name)
+        bs = mix64(self.seed ^ t)
+        ns = 0 if stream_idx == 0 else mix64(bs + stream_idx)
+        loader.synth_h2d(dst, 0, bs, self.base_std, ns, self.expert_std * stream_idx, stream)
+
+
+class ArraySink:
+    def __init__(self, out: Mapping):
+        self.out = out
+
+    def drain(self, loader: HostLoader, name: str, src: torch.Tensor, stream) -> None:
+        dst = self.out[name]
+        if isinstance(dst, torch.Tensor):
+            dst = dst.view(torch.int16).numpy() if dst.dtype == torch.bfloat16 else dst.numpy()
+        loader.d2h(dst.reshape(-1), src, stream)
+
+
+class ChecksumSink:
+    """Keeps a 64-bit checksum per tensor instead of the fused values (for outputs larger than RAM)."""
+
+    def __init__(self):
+        self.sums: dict[str, int] = {}
+
+    def drain(self, loader: HostLoader, name: str, src: torch.Tensor, stream) -> None:
+        nb = src.numel() * src.element_size()
+        main = nb - nb % 8
+        flat = src.view(torch.uint8)[:main] if main else None
+        s = loader.d2h_checksum(flat, stream) if main else 0
+        self.sums[name] = s
+
+
+# ----------------------------------------------------------------------------- driver
+@dataclass
+class StreamingReport:
+    stats: dict[str, FusionStats] = field(default_factory=dict)
+    groups: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+
+def plan_groups(numels: Sequence[int], n_experts: int, esize: int, budget_bytes: int) -> list[list[int]]:
+    """Consecutive tensor groups whose (N+1 inputs + output) bytes fit half the budget each."""
+    half = budget_bytes // 2
+    groups, cur, cur_b = [], [], 0
+    for t, n in enumerate(numels):
+        b = n * esize * (n_experts + 2)
+        if b > half:
+            raise ValueError(f"tensor {t} ({n} elements) does not fit half the device budget; raise the budget")
+        if cur and cur_b + b > half:
+            groups.append(cur)
+            cur, cur_b = [], 0
+        cur.append(t)
+        cur_b += b
+    if cur:
+        groups.append(cur)
+    return groups
+
+
+def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, source, sink,
+                   cfg: FusionConfig = FusionConfig(), dtype: torch.dtype = torch.bfloat16,
+                   device_budget_bytes: int = 64 << 30, stats: bool = True,
+                   loader: HostLoader | None = None) -> StreamingReport:
+    """Fuse a host-resident (or synthesised) checkpoint through the device in double-buffered groups."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    esize = torch.tensor([], dtype=dtype).element_size()
+    groups = plan_groups(numels, n_experts, esize, device_budget_bytes)
+    own_loader = loader is None
+    loader = loader or HostLoader()
+    copy_s, comp_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    weights = cfg.merge_weights or tuple(1.0 / n_experts for _ in range(n_experts))
+    half_elems = (device_budget_bytes // 2) // esize
+    # two workspaces, each one flat buffer carved per group: (N+1) inputs + output
+    ws = [torch.empty(half_elems, dtype=dtype, device=dev) for _ in range(2)]
+    rep = StreamingReport(groups=len(groups))
+    pending = None  # (names, out views, compute-done event, call, tensor ids)
+    try:
+        for gi, group in enumerate(groups):
+            buf = ws[gi % 2]
+            # the previous user of this workspace must have drained (its D2H ran on copy_s, in order)
+            off = 0
+            pieces, outs = [], []
+            for k, t in enumerate(group):
+                n = numels[t]
+                views = []
+                for _ in range(n_experts + 2):
+                    views.append(buf[off:off + n])
+                    off += (n + 63) // 64 * 64  # keep 128-byte alignment
+                for si in range(n_experts + 1):
+                    source.fill(loader, names[t], si, views[si], copy_s)
+                    rep.h2d_bytes += n * esize
+                pieces.append(Piece(k, 0, views[0], views[1:n_experts + 1], views[-1]))
+                outs.append(views[-1])
+            ready = torch.cuda.Event()
+            ready.record(copy_s)
+            comp_s.wait_event(ready)
+            call = FusionCall(pieces, FusionLayout([numels[t] for t in group]), n_experts, cfg, stream=comp_s)
+            call.run(weights)
+            done = torch.cuda.Event()
+            done.record(comp_s)
+            # drain the previous group while this one computes
+            if pending is not None:
+                _drain(pending, loader, sink, copy_s, names, rep, stats, weights)
+            pending = (group, outs, done, call)
+        if pending is not None:
+            _drain(pending, loader, sink, copy_s, names, rep, stats, weights)
+        torch.cuda.synchronize(dev)
+    finally:
+        if own_loader:
+            loader.close()
+    return rep
+
+
+def _drain(pending, loader, sink, copy_s, names, rep, stats, weights):
+    group, outs, done, call = pending
+    copy_s.wait_event(done)
+    for t, o in zip(group, outs):
+        sink.drain(loader, names[t], o, copy_s)
+        rep.d2h_bytes += o.numel() * o.element_size()
+    if stats:
+        for k, t in enumerate(group):
+            rep.stats[names[t]] = call.stats(k, weights)
