@@ -140,7 +140,7 @@ def plan_groups(numels: Sequence[int], n_experts: int, esize: int, budget_bytes:
     half = budget_bytes // 2
     groups, cur, cur_b = [], [], 0
     for t, n in enumerate(numels):
-        b = n * esize * (n_experts + 2)
+        b = (n + 63) // 64 * 64 * esize * (n_experts + 2)
         if b > half:
             raise ValueError(f"tensor {t} ({n} elements) does not fit half the device budget; raise the budget")
         if cur and cur_b + b > half:

@@ -16,7 +16,7 @@ def _host_bf16(d):
     return {k: torch.from_numpy(v.astype(np.float32)).to(torch.bfloat16) for k, v in d.items()}
 
 
-@pytest.mark.parametrize("budget", [4 << 20, 64 << 20])
+@pytest.mark.parametrize("budget", [16 << 20, 256 << 20])
 def test_streaming_equals_in_hbm(cuda, budget):
     from paper_2509_18883_b200 import fusion as F
     from paper_2509_18883_b200.loader import ArraySink, ArraySource, HostLoader, fuse_streaming
@@ -29,7 +29,7 @@ def test_streaming_equals_in_hbm(cuda, budget):
     rep = fuse_streaming(names, [hb[k].numel() for k in names], 3, ArraySource(hb, he), ArraySink(out), cfg,
                          device_budget_bytes=budget, loader=ld)
     ld.close()
-    assert rep.groups >= (2 if budget < (8 << 20) else 1)
+    assert rep.groups >= (2 if budget < (32 << 20) else 1)
     dev_out, drep = F.fuse_state_dict({k: v.to(cuda) for k, v in hb.items()},
                                       [{k: v.to(cuda) for k, v in e.items()} for e in he], cfg)
     for k in names:
@@ -51,6 +51,7 @@ def test_loader_roundtrip_and_checksum(cuda):
     ld.d2h(back, dst, s)
     assert np.array_equal(back, src)
     x = torch.arange(1 << 20, dtype=torch.int64, device=cuda)
+    torch.cuda.synchronize()  # produced on the default stream, read on s
     assert ld.d2h_checksum(x.view(torch.uint8), s) == sum(range(1 << 20))
     # synthesis: deterministic and base-consistent
     a = torch.empty(1 << 20, dtype=torch.bfloat16, device=cuda)
