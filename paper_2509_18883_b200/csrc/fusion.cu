@@ -611,6 +611,32 @@ __device__ __forceinline__ float mid_of(float y) {
 // Fast K3 for bf16 experts + bf16 base -> bf16 (the checkpoint path): f32x2 arithmetic with certified
 // guards; DROP 0 = no dropout, 2 = keep bits from the K2 bitmap; ERASE 0 off, 1 sum vote, 2 squared vote.
 // Elements whose guard trips are recomputed exactly (merge_elem_slow) in a rarely-taken phase 2.
+// Per-thread unit of the fast merge: kFastElems bf16 elements (kFastPairs 32-bit words) per stream.
+constexpr int kFastPairs = 2;
+constexpr int kFastElems = 2 * kFastPairs;
+struct FastVec {
+  uint32_t w[kFastPairs];
+  __device__ static FastVec load(const void* p) {
+    FastVec v;
+    if constexpr (kFastPairs == 4) {
+      const uint4 q = lds128(p);
+      v.w[0] = q.x; v.w[1] = q.y; v.w[2] = q.z; v.w[3] = q.w;
+    } else {
+      uint2 q;
+      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(q.x), "=r"(q.y) : "r"(smem_u32(p)));
+      v.w[0] = q.x; v.w[1] = q.y;
+    }
+    return v;
+  }
+  __device__ static void store(void* p, const uint32_t* w) {
+    if constexpr (kFastPairs == 4) {
+      stg128_stream(p, make_uint4(w[0], w[1], w[2], w[3]));
+    } else {
+      asm volatile("st.global.L1::no_allocate.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(w[0]), "r"(w[1]) : "memory");
+    }
+  }
+};
+
 template <int N, int DROP, int ERASE>
 __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_constant__ MergeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -659,29 +685,29 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
       mbar_wait(&r.full[s], ph);
       const uint8_t* sb = r.buf + s * r.stage_bytes;
       const uint8_t* bm = sb + (N + 1) * SB;
-      const uint32_t nvec = main_elems / 8;
+      const uint32_t nvec = main_elems / kFastElems;
       const uint64_t out_base = g.start + off;
       for (uint32_t v = fast_ok ? tid : nvec; v < nvec; v += kFastCThreads) {
-        const uint32_t le = v * 8;
-        const uint4 bw4 = lds128(sb + v * 16);
-        uint4 xw4[N];
+        const uint32_t le = v * kFastElems;
+        const FastVec bw4 = FastVec::load(sb + v * (2 * kFastElems));
+        FastVec xw4[N];
         uint32_t kb[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          xw4[i] = lds128(sb + (i + 1) * SB + v * 16);
-          kb[i] = DROP ? (uint32_t)bm[i * BMB + v] : 0xffu;
+          xw4[i] = FastVec::load(sb + (i + 1) * SB + v * (2 * kFastElems));
+          kb[i] = DROP ? ((uint32_t)bm[i * BMB + (le >> 3)] >> (le & 7)) : 0xffu;
         }
-        uint32_t outw[4];
+        uint32_t outw[kFastPairs];
         uint32_t slowm = 0;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const uint32_t bw = word_of(bw4, p);
+        for (int p = 0; p < kFastPairs; ++p) {
+          const uint32_t bw = bw4.w[p];
           const float2 b2 = make_float2(bf16_lo(bw), bf16_hi(bw));
           float2 k2[N];
           float2 aa = make_float2(0.f, 0.f);
 #pragma unroll
           for (int i = 0; i < N; ++i) {
-            const uint32_t xw = word_of(xw4[i], p);
+            const uint32_t xw = xw4[i].w[p];
             const float2 d2 = __ffma2_rn(b2, make_float2(-1.f, -1.f), make_float2(bf16_lo(xw), bf16_hi(xw)));
             if (DROP) {
               const float2 m2 = make_float2(((kb[i] >> (2 * p)) & 1u) ? sr32[i] : 0.f,
@@ -745,15 +771,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
         }
         if (slowm) {  // phase 2 (rare): exact reference-order evaluation of flagged elements
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
+          for (int e = 0; e < kFastElems; ++e) {
             if ((slowm >> e) & 1u) {
-              const uint32_t bw = word_of(bw4, e >> 1);
+              const uint32_t bw = bw4.w[e >> 1];
               const float be = (e & 1) ? bf16_hi(bw) : bf16_lo(bw);
               FArr<N> xe;
               uint32_t keep = 0;
 #pragma unroll
               for (int i = 0; i < N; ++i) {
-                const uint32_t xw = word_of(xw4[i], e >> 1);
+                const uint32_t xw = xw4[i].w[e >> 1];
                 xe.v[i] = (e & 1) ? bf16_hi(xw) : bf16_lo(xw);
                 keep |= ((kb[i] >> e) & 1u) << i;
               }
@@ -770,7 +796,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
             }
           }
         }
-        stg128_stream(outp + out_base + le, make_uint4(outw[0], outw[1], outw[2], outw[3]));
+        FastVec::store(outp + out_base + le, outw);
       }
       // items the fast path cannot certify, and the < 16-byte tail: exact f64 path
       const uint32_t e0 = fast_ok ? main_elems : 0;

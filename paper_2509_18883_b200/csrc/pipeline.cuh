@@ -13,7 +13,7 @@ constexpr int kThreads = kCThreads + 32;
 __device__ __forceinline__ void cbar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory"); }
 
 // K3 fast path consumer warps (8: more forces <= 128 registers and spills)
-constexpr int kFastCWarps = 8;
+constexpr int kFastCWarps = 16;
 constexpr int kFastCThreads = kFastCWarps * 32;
 constexpr int kFastThreads = kFastCThreads + 32;
 
