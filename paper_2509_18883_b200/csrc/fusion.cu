@@ -284,6 +284,102 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ S
   }
 }
 
+// K1 for bf16 pair-mode inputs: exact f64 squares of (expert - base) with the bf16 -> f64 widening
+// done once for the base and once per expert (F2F on the XU pipe), two independent f64 accumulator
+// chains per expert, and the non-zero-after-dropout count as popc(neq_bits & keep_bits) per vector.
+// COUNT: 0 no counting, 1 no dropout (every entry kept), 2 keep bits from the K2 bitmap.
+template <int N, int COUNT>
+__global__ void __launch_bounds__(kThreads, 2) k_sumsq_bf16(const __grid_constant__ SumsqArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr uint32_t SB = StreamBytes<N>::v;
+  constexpr uint32_t ELEMS = SB / 2;
+  constexpr uint32_t BMB = ELEMS / 8;
+  const Ring r = ring_setup(smem, a.stage_bytes, a.nstages);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == kCWarps) {
+    if (lane == 0) produce<2, N>(a.plan, r, true, COUNT == 2 ? a.bitmap : nullptr, a.words_per_row);
+    return;
+  }
+  __shared__ double red[kCWarps][N];
+  const int tid = threadIdx.x;
+  uint32_t q = 0;
+  for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
+    const ItemGeom g = item_geom(a.plan, item);
+    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    double acc0[N], acc1[N];
+    uint32_t nz[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      acc0[i] = acc1[i] = 0.0;
+      nz[i] = 0;
+    }
+    for (uint32_t off = 0; off < g.len; off += ELEMS) {
+      const uint32_t n = min(ELEMS, g.len - off);
+      const uint32_t main_elems = ((n * 2) & ~15u) / 2;
+      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      mbar_wait(&r.full[s], ph);
+      const uint8_t* sb = r.buf + s * r.stage_bytes;
+      const uint8_t* bm = sb + (N + 1) * SB;
+      const uint32_t nvec = main_elems / 8;
+      for (uint32_t v = tid; v < nvec; v += kCThreads) {
+        float bf[8];
+        VecIO<RLK_BF16>::f32(lds128(sb + v * 16), bf);
+        double bd[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) bd[e] = (double)bf[e];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          float xf[8];
+          VecIO<RLK_BF16>::f32(lds128(sb + (i + 1) * SB + v * 16), xf);
+          uint32_t neq = 0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const double d = (double)xf[e] - bd[e];
+            if (e & 1) acc1[i] = fma(d, d, acc1[i]);
+            else acc0[i] = fma(d, d, acc0[i]);
+            if (COUNT) neq |= (xf[e] != bf[e]) ? (1u << e) : 0u;
+          }
+          if (COUNT == 1) nz[i] += __popc(neq);
+          if (COUNT == 2) nz[i] += __popc(neq & (uint32_t)bm[i * BMB + v]);
+        }
+      }
+      for (uint32_t e = main_elems + tid; e < n; e += kCThreads) {
+        const uint64_t idx = g.start + off + e;
+        const double b = load_f64<RLK_BF16>(g.seg->base, idx);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double d = load_f64<RLK_BF16>(g.seg->expert[i], idx) - b;
+          acc0[i] = fma(d, d, acc0[i]);
+          if (COUNT) {
+            const bool keep = COUNT == 1 || keep_draw(a.seed[i], jtensor0 + off + e, a.thresh);
+            nz[i] += keep && (d != 0.0);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r.empty[s]);
+      ++q;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double w = warp_sum_f64(acc0[i] + acc1[i]);
+      if (lane == 0) red[warp][i] = w;
+      if (COUNT) {
+        const uint32_t z = __reduce_add_sync(0xffffffffu, nz[i]);
+        if (lane == 0 && z) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + i, (unsigned long long)z);
+      }
+    }
+    cbar_sync();
+    if (tid < N) {
+      double t = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kCWarps; ++w) t += red[w][tid];
+      a.partials[(uint64_t)g.gitem * N + tid] = t;
+    }
+    cbar_sync();
+  }
+}
+
 // ------------------------------------------------------------------ finalize: norms -> scales
 // One warp per tensor; lane l sums items l, l+32, ... then a fixed xor-tree: the result depends only
 // on the global item partition, never on which rank produced which partial.
@@ -857,6 +953,12 @@ static int launch_sumsq(SumsqArgs& a, cudaStream_t s) {
   a.nstages = ns;
   const uint32_t smem = 1024 + sb * ns;
   auto kern = k_sumsq<DT, N>;
+  if constexpr (DT == RLK_BF16 && N <= 4) {
+    // pair mode with no inline dropout draws: the bf16 fast kernel
+    if (!a.delta_mode && !(a.counters && a.dropout_mode == 1)) {
+      kern = !a.counters ? k_sumsq_bf16<N, 0> : (a.dropout_mode == 2 ? k_sumsq_bf16<N, 2> : k_sumsq_bf16<N, 1>);
+    }
+  }
   int st = ensure_smem(kern, smem);
   if (st) return st;
   uint32_t grid = std::min<uint32_t>(a.plan.n_items, 2u * (uint32_t)sm_count());
