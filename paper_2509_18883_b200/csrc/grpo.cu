@@ -19,6 +19,12 @@ namespace rlk {
 
 constexpr uint32_t kRowStageBytes = 32768;
 constexpr uint32_t kRowStages = 6;
+// 16 consumer warps + 1 producer warp: the per-logit chain (max, FFMA, MUFU.EX2, FADD) is short, so
+// latency hiding needs warps (profiles/r01: 8 warps gave IPC 1.6 and 52% of HBM peak)
+constexpr int kGW = 16;
+constexpr int kGT = kGW * 32;
+constexpr int kGThreads = kGT + 32;
+__device__ __forceinline__ void gbar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kGT) : "memory"); }
 constexpr double kLog2e = 1.4426950408889634074;
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -97,7 +103,7 @@ template <int DT>
 __device__ double row_lse_global(const char* rowp, uint64_t V, double T, double* red_m, double* red_s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double m = -INFINITY, sum = 0.0;
-  for (uint64_t v = threadIdx.x; v < V; v += kCThreads) {
+  for (uint64_t v = threadIdx.x; v < V; v += kGT) {
     const double z = load_f64<DT>(rowp, v);
     const double zt = T == 1.0 ? z : __ddiv_rn(z, T);
     if (zt > m) { sum = sum * exp(m - zt); m = zt; }
@@ -111,12 +117,12 @@ __device__ double row_lse_global(const char* rowp, uint64_t V, double T, double*
     m = M;
   }
   if (lane == 0) { red_m[warp] = m; red_s[warp] = sum; }
-  cbar_sync();
+  gbar_sync();
   double M = red_m[0];
-  for (int w = 1; w < kCWarps; ++w) M = fmax(M, red_m[w]);
+  for (int w = 1; w < kGW; ++w) M = fmax(M, red_m[w]);
   double S = 0.0;
-  for (int w = 0; w < kCWarps; ++w) S += red_m[w] == -INFINITY ? 0.0 : red_s[w] * exp(red_m[w] - M);
-  cbar_sync();
+  for (int w = 0; w < kGW; ++w) S += red_m[w] == -INFINITY ? 0.0 : red_s[w] * exp(red_m[w] - M);
+  gbar_sync();
   return M + log(S);
 }
 
@@ -167,11 +173,11 @@ __device__ void fwd_epilogue(const FwdArgs& a, uint64_t row, const char* rowp, d
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd(FwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DT>::size;
   constexpr int VEC = 16 / ESZ;
-  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages);
+  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages, kGW);
   const uint64_t row_bytes = a.vocab * ESZ;
   auto active = [&](uint64_t row) { return a.use[a.sample[row]] != 0; };
   auto addr = [&](uint64_t row) {
@@ -181,11 +187,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
   // rows whose start is not 16-byte aligned (tiny toy vocabularies) bypass the TMA ring
   auto streamed = [&](uint64_t row) { return active(row) && ((uintptr_t)addr(row) & 15u) == 0; };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  if (warp == kCWarps) {
+  if (warp == kGW) {
     if (lane == 0) produce_rows(r, a.n_rows, row_bytes, streamed, addr);
     return;
   }
-  __shared__ double red_m[kCWarps], red_s[kCWarps];
+  __shared__ double red_m[kGW], red_s[kGW];
   uint32_t q = 0;
   for (uint64_t row = blockIdx.x; row < a.n_rows; row += gridDim.x) {
     if (!active(row)) {
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
         const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
         mbar_wait(&r.full[s], ph);
         const uint8_t* sb = r.buf + s * r.stage_bytes;
-        for (uint32_t v = tid; v < main_bytes / 16; v += kCThreads) {
+        for (uint32_t v = tid; v < main_bytes / 16; v += kGT) {
           double z[2];
           RowVec<RLK_F64>::f64(lds128(sb + v * 16), z);
 #pragma unroll
@@ -221,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
             sum += exp(zt - m);
           }
         }
-        for (uint32_t e = main_bytes / 8 + tid; e < bytes / 8; e += kCThreads) {
+        for (uint32_t e = main_bytes / 8 + tid; e < bytes / 8; e += kGT) {
           const double z = load_f64<DT>(rowp, off / 8 + e);
           const double zt = T == 1.0 ? z : __ddiv_rn(z, T);
           if (zt > m) { sum = sum * exp(m - zt); m = zt; }
@@ -239,17 +245,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
         m = M;
       }
       if (lane == 0) { red_m[warp] = m; red_s[warp] = sum; }
-      cbar_sync();
+      gbar_sync();
       double M = red_m[0];
-      for (int w = 1; w < kCWarps; ++w) M = fmax(M, red_m[w]);
+      for (int w = 1; w < kGW; ++w) M = fmax(M, red_m[w]);
       double S = 0.0;
-      for (int w = 0; w < kCWarps; ++w) S += red_m[w] == -INFINITY ? 0.0 : red_s[w] * exp(red_m[w] - M);
+      for (int w = 0; w < kGW; ++w) S += red_m[w] == -INFINITY ? 0.0 : red_s[w] * exp(red_m[w] - M);
       lse = M + log(S);
-      cbar_sync();
+      gbar_sync();
     } else {
       // f32 path in the log2 domain: x = z * c, c = log2(e) / T; one MUFU.EX2 per logit.
       const float c = (float)(kLog2e / T);
-      float mz = -INFINITY, sum = 0.f, nb = INFINITY;
+      float mz = -INFINITY, sum = 0.f, sum2 = 0.f, nb = INFINITY;
       for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
         const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
         const uint32_t main_bytes = bytes & ~15u;
@@ -257,24 +263,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
         mbar_wait(&r.full[s], ph);
         const uint8_t* sb = r.buf + s * r.stage_bytes;
         const uint32_t nvec = main_bytes / 16;
-        for (uint32_t v = tid; v < nvec; v += kCThreads) {
+        for (uint32_t v = tid; v < nvec; v += kGT) {
           float z[VEC];
           RowVec<DT>::f32(lds128(sb + v * 16), z);
-          float lm = z[0];
+          float lm = fmaxf(z[0], z[1]);
 #pragma unroll
-          for (int e = 1; e < VEC; ++e) lm = fmaxf(lm, z[e]);
-          if (lm > mz) {
-            sum *= ex2_approx((mz - lm) * c);
+          for (int e = 2; e < VEC; e += 2) lm = fmaxf(lm, fmaxf(z[e], z[e + 1]));
+          if (lm > mz) {  // new running max: rescale (rare after the first vectors of a row)
+            const float f = ex2_approx((mz - lm) * c);
+            sum *= f;
+            sum2 *= f;
             mz = lm;
             nb = -mz * c;
           }
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) sum += ex2_approx(fmaf(z[e], c, nb));
+          for (int e = 0; e < VEC; e += 2) {
+            sum += ex2_approx(fmaf(z[e], c, nb));
+            sum2 += ex2_approx(fmaf(z[e + 1], c, nb));
+          }
         }
-        for (uint32_t e = main_bytes / ESZ + tid; e < bytes / ESZ; e += kCThreads) {
+        for (uint32_t e = main_bytes / ESZ + tid; e < bytes / ESZ; e += kGT) {
           const float z = (float)load_f64<DT>(rowp, off / ESZ + e);
           if (z > mz) {
-            sum *= ex2_approx((mz - z) * c);
+            const float f = ex2_approx((mz - z) * c);
+            sum *= f;
+            sum2 *= f;
             mz = z;
             nb = -mz * c;
           }
@@ -284,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
         if (lane == 0) mbar_arrive(&r.empty[s]);
         ++q;
       }
+      sum += sum2;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const float om = __shfl_xor_sync(0xffffffffu, mz, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
@@ -292,15 +306,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_fwd(FwdArgs a) {
         mz = M;
       }
       if (lane == 0) { red_m[warp] = mz; red_s[warp] = sum; }
-      cbar_sync();
+      gbar_sync();
       double M = red_m[0];
-      for (int w = 1; w < kCWarps; ++w) M = fmax(M, red_m[w]);
+      for (int w = 1; w < kGW; ++w) M = fmax(M, red_m[w]);
       double S = 0.0;
-      for (int w = 0; w < kCWarps; ++w)
+      for (int w = 0; w < kGW; ++w)
         S += red_m[w] == -INFINITY ? 0.0 : red_s[w] * exp2((red_m[w] - M) * (kLog2e / T));
       // lse of z/T (natural log): max/T + ln(S)
       lse = (T == 1.0 ? M : M / T) + log(S);
-      cbar_sync();
+      gbar_sync();
     }
     if (tid == 0) fwd_epilogue<DT>(a, row, rowp, lse);
   }
@@ -355,13 +369,13 @@ __device__ __forceinline__ void store_grad_f32(char* g, uint64_t idx, const floa
 }
 
 template <int DT, int GT>
-__global__ void __launch_bounds__(kThreads, 1) k_grpo_bwd(BwdArgs a) {
+__global__ void __launch_bounds__(kGThreads, 1) k_grpo_bwd(BwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DT>::size;
   constexpr int GSZ = Elem<GT>::size;
   constexpr int VEC = 16 / ESZ;
   constexpr bool F64MATH = (DT == RLK_F64) || (GT == RLK_F64);
-  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages);
+  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages, kGW);
   const uint64_t row_bytes = a.vocab * ESZ;
   auto lrow = [&](uint64_t o) { return a.logits_row ? (uint64_t)a.logits_row[o] : o; };
   auto active = [&](uint64_t o) {
@@ -374,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_bwd(BwdArgs a) {
   auto addr = [&](uint64_t o) { return a.logits + lrow(o) * a.row_stride * ESZ; };
   auto streamed = [&](uint64_t o) { return active(o) && ((uintptr_t)addr(o) & 15u) == 0; };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  if (warp == kCWarps) {
+  if (warp == kGW) {
     if (lane == 0) produce_rows(r, a.n_out_rows, row_bytes, streamed, addr);
     return;
   }
@@ -385,20 +399,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_bwd(BwdArgs a) {
       // objective.py:275-276 leaves the row at zero
       const uint64_t gbytes = a.vocab * GSZ;
       if (((uintptr_t)grow & 15u) == 0) {
-        for (uint64_t b = (uint64_t)tid * 16; b + 16 <= gbytes; b += kCThreads * 16)
+        for (uint64_t b = (uint64_t)tid * 16; b + 16 <= gbytes; b += kGT * 16)
           stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
-        for (uint64_t b = (gbytes & ~15ull) + tid; b < gbytes; b += kCThreads) grow[b] = 0;
+        for (uint64_t b = (gbytes & ~15ull) + tid; b < gbytes; b += kGT) grow[b] = 0;
       } else {
-        for (uint64_t b = tid; b < gbytes; b += kCThreads) grow[b] = 0;
+        for (uint64_t b = tid; b < gbytes; b += kGT) grow[b] = 0;
       }
       continue;
     }
     int64_t k0, k1;
     tok_range(a, o, k0, k1);
     const char* rowp = addr(o);
+    float rc_cf = 0.f, rc_c = 0.f, rc_nl = 0.f;
+    int64_t rc_tok = -1;
+    if (!F64MATH && a.row_tok_ptr == nullptr) {
+      const double T = a.temp[o];
+      rc_cf = (float)a.coef[o];
+      rc_c = (float)(kLog2e / T);
+      rc_nl = (float)(-a.lse[o] * kLog2e);
+      rc_tok = a.tokens[o];
+    }
     if (((uintptr_t)rowp & 15u) != 0 || ((uintptr_t)grow & 15u) != 0) {
       // unaligned row: reference-order f64 evaluation straight from global memory
-      for (uint64_t v = tid; v < a.vocab; v += kCThreads) {
+      for (uint64_t v = tid; v < a.vocab; v += kGT) {
         const double z = load_f64<DT>(rowp, v);
         double g = 0.0;
         for (int64_t k = k0; k < k1; ++k) {
@@ -422,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_bwd(BwdArgs a) {
       const uint8_t* sb = r.buf + s * r.stage_bytes;
       const uint64_t v0 = off / ESZ;  // first vocab index of this stage
       const uint32_t nvec = main_bytes / 16;
-      for (uint32_t v = tid; v < nvec + ((bytes - main_bytes) ? 1u : 0u); v += kCThreads) {
+      for (uint32_t v = tid; v < nvec + ((bytes - main_bytes) ? 1u : 0u); v += kGT) {
         const bool tail = v >= nvec;
         const int n = tail ? (int)((bytes - main_bytes) / ESZ) : VEC;
         const uint64_t vb = v0 + (uint64_t)v * VEC;
@@ -459,6 +482,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_grpo_bwd(BwdArgs a) {
             }
           }
           for (int e = 0; e < n; ++e) store_from_f64<GT>(grow, vb + e, g[e]);
+        } else if (a.row_tok_ptr == nullptr) {
+          // one token per row (the LM layout): row constants in registers, one-hot patched once
+          float z[VEC], g[VEC];
+          if (!tail) RowVec<DT>::f32(lds128(sb + v * 16), z);
+          else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) z[e] = e < n ? (float)load_f64<DT>(rowp, vb + e) : 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; e += 2) {
+            g[e] = -rc_cf * ex2_approx(fmaf(z[e], rc_c, rc_nl));
+            g[e + 1] = -rc_cf * ex2_approx(fmaf(z[e + 1], rc_c, rc_nl));
+          }
+          const int64_t rel = rc_tok - (int64_t)vb;
+          if (rel >= 0 && rel < VEC) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+              if (e == rel) g[e] += rc_cf;
+          }
+          store_grad_f32<GT>(grow, vb, g, n);
         } else {
           float z[VEC], g[VEC];
 #pragma unroll
@@ -560,7 +603,7 @@ static int launch_fwd(const FwdArgs& a, cudaStream_t s) {
   const uint32_t smem = 1024 + kRowStageBytes * kRowStages;
   auto kern = k_grpo_fwd<DT>;
   if (int st = set_smem(kern, smem)) return st;
-  kern<<<grid_rows(a.n_rows), kThreads, smem, s>>>(a);
+  kern<<<grid_rows(a.n_rows), kGThreads, smem, s>>>(a);
   return launch_status("rlk_grpo_fwd");
 }
 
@@ -569,7 +612,7 @@ static int launch_bwd(const BwdArgs& a, cudaStream_t s) {
   const uint32_t smem = 1024 + kRowStageBytes * kRowStages;
   auto kern = k_grpo_bwd<DT, GT>;
   if (int st = set_smem(kern, smem)) return st;
-  kern<<<grid_rows(a.n_out_rows), kThreads, smem, s>>>(a);
+  kern<<<grid_rows(a.n_out_rows), kGThreads, smem, s>>>(a);
   return launch_status("rlk_grpo_bwd");
 }
 
