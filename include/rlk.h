@@ -118,7 +118,10 @@ int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, i
  * Rows of masked samples are not read (objective.py:240-241).
  * Outputs per token (device, f64): logp (z_tok/T - lse), lse (natural log-sum-exp of z/T), term
  * (w * value, 0 if masked) and coef (norm * w * slope * r / T, the dJ/dlogit scale; 0 if masked).
- * flags[0] |= 1 when a row's logp is non-finite, |= 2 when a token id is out of [0, V).  Caller zeroes. */
+ * flags[0] |= 1 when a row's logp is non-finite, |= 2 when a token id is out of [0, V).  Caller zeroes.
+ * workspace (device f32, >= n_rows * 32 floats, nullable): with it, bf16/f32 logits run as two kernels
+ * (K4a streams rows and writes per-(row, warp) log-sum-exp partials without block synchronisation;
+ * K4b combines them and runs the epilogue); without it, one kernel reduces each row in-block. */
 typedef struct rlk_clip {
   double eps_neg_low, eps_pos_high, eps_neg_high, tis_cap;
   int32_t guard_positive;
@@ -129,7 +132,7 @@ int rlk_grpo_fwd(const void* logits, int dtype, uint64_t n_rows, uint64_t vocab,
                  const double* logp_infer, const int32_t* sample_of_row, const double* adv,
                  const uint8_t* use, const double* temperature, const double* norm,
                  const rlk_clip* clip, double* logp_out, double* lse_out, double* term,
-                 double* coef, int32_t* flags, void* stream);
+                 double* coef, int32_t* flags, float* workspace, uint64_t workspace_floats, void* stream);
 
 /* out[g] = sum of x[seg_ptr[g] .. seg_ptr[g+1]) in a fixed order (one warp per segment). */
 int rlk_segment_sum_f64(const double* x, const int64_t* seg_ptr, uint64_t n_segs, double* out, void* stream);

@@ -320,6 +320,125 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd(FwdArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ K4 split form (bf16 / f32)
+// K4a streams every row and leaves per-(row, warp) partials (max z, sum 2^((z - max) c)) in a
+// workspace -- no block-level synchronisation anywhere in the streaming loop; K4b combines the
+// kGW partials of a row in f64 and runs the epilogue, one thread per row.
+template <int DT>
+__global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd_stream(FwdArgs a, float* __restrict__ ws) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int ESZ = Elem<DT>::size;
+  constexpr int VEC = 16 / ESZ;
+  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages, kGW);
+  const uint64_t row_bytes = a.vocab * ESZ;
+  auto active = [&](uint64_t row) { return a.use[a.sample[row]] != 0; };
+  auto addr = [&](uint64_t row) {
+    const uint64_t rr = a.row_index ? (uint64_t)a.row_index[row] : row;
+    return a.logits + rr * a.row_stride * ESZ;
+  };
+  auto streamed = [&](uint64_t row) { return active(row) && ((uintptr_t)addr(row) & 15u) == 0; };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  if (warp == kGW) {
+    if (lane == 0) produce_rows(r, a.n_rows, row_bytes, streamed, addr);
+    return;
+  }
+  uint32_t q = 0;
+  for (uint64_t row = blockIdx.x; row < a.n_rows; row += gridDim.x) {
+    if (!active(row)) continue;
+    const char* rowp = addr(row);
+    const float c = (float)(kLog2e / a.temp[a.sample[row]]);
+    float mz = -INFINITY, sum = 0.f, sum2 = 0.f, nb = INFINITY;
+    auto take = [&](float z) {
+      if (z > mz) {
+        const float f = ex2_approx((mz - z) * c);
+        sum *= f;
+        sum2 *= f;
+        mz = z;
+        nb = -mz * c;
+      }
+      sum += ex2_approx(fmaf(z, c, nb));
+    };
+    if (((uintptr_t)rowp & 15u) != 0) {
+      for (uint64_t v = tid; v < a.vocab; v += kGT) take((float)load_f64<DT>(rowp, v));
+    } else {
+      for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
+        const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
+        const uint32_t main_bytes = bytes & ~15u;
+        const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+        mbar_wait(&r.full[s], ph);
+        const uint8_t* sb = r.buf + s * r.stage_bytes;
+        const uint32_t nvec = main_bytes / 16;
+        for (uint32_t v = tid; v < nvec; v += kGT) {
+          float z[VEC];
+          RowVec<DT>::f32(lds128(sb + v * 16), z);
+          float lm = fmaxf(z[0], z[1]);
+#pragma unroll
+          for (int e = 2; e < VEC; e += 2) lm = fmaxf(lm, fmaxf(z[e], z[e + 1]));
+          if (lm > mz) {
+            const float f = ex2_approx((mz - lm) * c);
+            sum *= f;
+            sum2 *= f;
+            mz = lm;
+            nb = -mz * c;
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; e += 2) {
+            sum += ex2_approx(fmaf(z[e], c, nb));
+            sum2 += ex2_approx(fmaf(z[e + 1], c, nb));
+          }
+        }
+        for (uint32_t e = main_bytes / ESZ + tid; e < bytes / ESZ; e += kGT)
+          take((float)load_f64<DT>(rowp, off / ESZ + e));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&r.empty[s]);
+        ++q;
+      }
+    }
+    sum += sum2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, mz, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
+      const float M = fmaxf(mz, om);
+      sum = (M == -INFINITY) ? 0.f : sum * ex2_approx((mz - M) * c) + os * ex2_approx((om - M) * c);
+      mz = M;
+    }
+    if (lane == 0) {
+      ws[(row * kGW + warp) * 2] = mz;
+      ws[(row * kGW + warp) * 2 + 1] = sum;
+    }
+  }
+}
+
+template <int DT>
+__global__ void k_grpo_fwd_epilogue(FwdArgs a, const float* __restrict__ ws) {
+  constexpr int ESZ = Elem<DT>::size;
+  for (uint64_t row = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; row < a.n_rows;
+       row += (uint64_t)gridDim.x * blockDim.x) {
+    if (a.use[a.sample[row]] == 0) {
+      if (a.logp) a.logp[row] = 0.0;
+      if (a.lse) a.lse[row] = 0.0;
+      a.term[row] = 0.0;
+      a.coef[row] = 0.0;
+      continue;
+    }
+    const double T = a.temp[a.sample[row]];
+    const float2* pw = reinterpret_cast<const float2*>(ws + row * kGW * 2);
+    float2 pr[kGW];
+#pragma unroll
+    for (int w = 0; w < kGW; ++w) pr[w] = pw[w];
+    double M = pr[0].x;
+#pragma unroll
+    for (int w = 1; w < kGW; ++w) M = fmax(M, (double)pr[w].x);
+    double S = 0.0;
+#pragma unroll
+    for (int w = 0; w < kGW; ++w)
+      S += pr[w].x == -INFINITY ? 0.0 : (double)pr[w].y * exp2(((double)pr[w].x - M) * (kLog2e / T));
+    const double lse = (T == 1.0 ? M : M / T) + log(S);  // lse of z / T (toy_env.py:172-174)
+    const uint64_t rr = a.row_index ? (uint64_t)a.row_index[row] : row;
+    fwd_epilogue<DT>(a, row, a.logits + rr * a.row_stride * ESZ, lse);
+  }
+}
+
 // ------------------------------------------------------------------ K5 backward
 struct BwdArgs {
   const char* logits;
@@ -599,6 +718,18 @@ static int set_smem(K kern, uint32_t bytes) {
 }
 
 template <int DT>
+static int launch_fwd_split(const FwdArgs& a, float* ws, cudaStream_t s) {
+  const uint32_t smem = 1024 + kRowStageBytes * kRowStages;
+  auto kern = k_grpo_fwd_stream<DT>;
+  if (int st = set_smem(kern, smem)) return st;
+  kern<<<grid_rows(a.n_rows), kGThreads, smem, s>>>(a, ws);
+  if (int st = launch_status("rlk_grpo_fwd (stream)")) return st;
+  const uint64_t blocks = (a.n_rows + 255) / 256;
+  k_grpo_fwd_epilogue<DT><<<(unsigned)std::min<uint64_t>(blocks, 65535u * 16), 256, 0, s>>>(a, ws);
+  return launch_status("rlk_grpo_fwd (epilogue)");
+}
+
+template <int DT>
 static int launch_fwd(const FwdArgs& a, cudaStream_t s) {
   const uint32_t smem = 1024 + kRowStageBytes * kRowStages;
   auto kern = k_grpo_fwd<DT>;
@@ -651,7 +782,7 @@ int rlk_grpo_fwd(const void* logits, int dtype, uint64_t n_rows, uint64_t vocab,
                  const int64_t* row_index, const int32_t* tokens, const double* logp_train, const double* logp_infer,
                  const int32_t* sample_of_row, const double* adv, const uint8_t* use, const double* temperature,
                  const double* norm, const rlk_clip* clip, double* logp_out, double* lse_out, double* term,
-                 double* coef, int32_t* flags, void* stream) {
+                 double* coef, int32_t* flags, float* workspace, uint64_t workspace_floats, void* stream) {
   if (n_rows == 0) return RLK_OK;
   RLK_REQUIRE(logits && tokens && logp_train && logp_infer && sample_of_row && adv && use && temperature && norm &&
                   clip && term && coef && flags,
@@ -681,9 +812,10 @@ int rlk_grpo_fwd(const void* logits, int dtype, uint64_t n_rows, uint64_t vocab,
   a.coef = coef;
   a.flags = flags;
   cudaStream_t s = (cudaStream_t)stream;
+  const bool split = workspace && workspace_floats >= n_rows * 2 * (uint64_t)kGW && dtype != RLK_F64;
   switch (dtype) {
-    case RLK_BF16: return launch_fwd<RLK_BF16>(a, s);
-    case RLK_F32: return launch_fwd<RLK_F32>(a, s);
+    case RLK_BF16: return split ? launch_fwd_split<RLK_BF16>(a, workspace, s) : launch_fwd<RLK_BF16>(a, s);
+    case RLK_F32: return split ? launch_fwd_split<RLK_F32>(a, workspace, s) : launch_fwd<RLK_F32>(a, s);
     default: return launch_fwd<RLK_F64>(a, s);
   }
 }

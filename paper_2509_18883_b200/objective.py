@@ -179,6 +179,8 @@ def apply_masks(groups: Sequence[Group], t_max: int, rep_cfg: RepetitionConfig =
 
 
 # ----------------------------------------------------------------------------- tensor API
+GRPO_WS_FLOATS_PER_ROW = 32  # K4a partials: (max, sum) per consumer warp (include/rlk.h)
+
 @dataclass
 class GRPOBatch:
     """Packed device-side description of a token batch (rows grouped by sample, samples by group).
@@ -270,10 +272,11 @@ def grpo_forward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = Clip
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     s = L.stream_handle(stream)
     c = clip.c_struct()
+    ws = torch.empty(R * GRPO_WS_FLOATS_PER_ROW, dtype=torch.float32, device=dev)
     L.call("rlk_grpo_fwd", L.ptr(logits), L.dtype_code(logits.dtype), R, V, V, L.ptr(batch.row_index),
            L.ptr(batch.tokens), L.ptr(batch.logp_train), L.ptr(batch.logp_infer), L.ptr(batch.sample_of_row),
            L.ptr(batch.adv), L.ptr(batch.use), L.ptr(batch.temperature), L.ptr(batch.norm), L.C.byref(c),
-           L.ptr(logp), L.ptr(lse), L.ptr(term), L.ptr(coef), L.ptr(flags), s)
+           L.ptr(logp), L.ptr(lse), L.ptr(term), L.ptr(coef), L.ptr(flags), L.ptr(ws), ws.numel(), s)
     gs = torch.empty(batch.n_groups, **f64)
     L.call("rlk_segment_sum_f64", L.ptr(term), L.ptr(batch.group_rows), batch.n_groups, L.ptr(gs), s)
     if group is not None:
