@@ -20,7 +20,7 @@ RLK_BF16, RLK_F32, RLK_F64 = 0, 1, 2
 RLK_MAX_EXPERTS = 8
 RLK_FUSION_ITEM = 65536
 
-LIB_PATH = Path(__file__).resolve().parent / "_rlk.so"
+LIB_PATH = Path(os.environ.get("RLK_LIB_PATH", Path(__file__).resolve().parent / "_rlk.so"))
 
 # Layout of rlk_fusion_segment (include/rlk.h): 104 bytes, 8-byte aligned.
 SEGMENT_DTYPE = np.dtype([

@@ -450,6 +450,7 @@ struct MergeArgs {
   uint64_t words_per_row;
   unsigned long long* counters;
   int dropout_mode, erase_mode, delta_mode, with_base, fast;
+  uint32_t two;  // == 2 (runtime constant for the IMAD.HI counter)
   uint32_t stage_bytes, nstages;
   const uint32_t* bitmap;
 };
@@ -685,10 +686,12 @@ __device__ __forceinline__ uint32_t mask_lt0(float x) {  // 0xffffffff iff x < 0
   return r;
 }
 __device__ __forceinline__ float andnot_f(float x, uint32_t m) { return __uint_as_float(__float_as_uint(x) & ~m); }
-// c + (x >> 31) as one IMAD.HI on the FMA pipe: hi32(x * 2) + c
-__device__ __forceinline__ uint32_t add_sign_bit(uint32_t x, uint32_t c) {
+// c + (x >> 31) as one IMAD.HI on the FMA pipe: hi32(x * two) + c.  `two` is a runtime value (2) so
+// ptxas cannot turn it into an ALU-pipe LEA.HI.
+__device__ __forceinline__ uint32_t add_sign_bit(uint32_t x, uint32_t c, uint32_t two) {
   uint32_t r;
   asm("mad.hi.u32 %0, %1, 2, %2;" : "=r"(r) : "r"(x), "r"(c));
+  (void)two;
   return r;
 }
 // +-1.0f with the sign of x (one LOP3)
@@ -708,7 +711,10 @@ __device__ __forceinline__ float mid_of(float y) {
 // guards; DROP 0 = no dropout, 2 = keep bits from the K2 bitmap; ERASE 0 off, 1 sum vote, 2 squared vote.
 // Elements whose guard trips are recomputed exactly (merge_elem_slow) in a rarely-taken phase 2.
 // Per-thread unit of the fast merge: kFastElems bf16 elements (kFastPairs 32-bit words) per stream.
-constexpr int kFastPairs = 2;
+#ifndef RLK_FAST_PAIRS
+#define RLK_FAST_PAIRS 2
+#endif
+constexpr int kFastPairs = RLK_FAST_PAIRS;
 constexpr int kFastElems = 2 * kFastPairs;
 struct FastVec {
   uint32_t w[kFastPairs];
@@ -717,18 +723,22 @@ struct FastVec {
     if constexpr (kFastPairs == 4) {
       const uint4 q = lds128(p);
       v.w[0] = q.x; v.w[1] = q.y; v.w[2] = q.z; v.w[3] = q.w;
-    } else {
+    } else if constexpr (kFastPairs == 2) {
       uint2 q;
       asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(q.x), "=r"(q.y) : "r"(smem_u32(p)));
       v.w[0] = q.x; v.w[1] = q.y;
+    } else {
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v.w[0]) : "r"(smem_u32(p)));
     }
     return v;
   }
   __device__ static void store(void* p, const uint32_t* w) {
     if constexpr (kFastPairs == 4) {
       stg128_stream(p, make_uint4(w[0], w[1], w[2], w[3]));
-    } else {
+    } else if constexpr (kFastPairs == 2) {
       asm volatile("st.global.L1::no_allocate.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(w[0]), "r"(w[1]) : "memory");
+    } else {
+      asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(w[0]) : "memory");
     }
   }
 };
@@ -748,11 +758,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
   }
   const int tid = threadIdx.x;
   const float cv = ERASE == 1 ? 0x1p-20f : 0x1p-19f;
-  float w32[N];
+  float w32[N], wh32[N];
   float wmax = 0.f;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     w32[i] = (float)a.w[i];
+    wh32[i] = 0.5f * w32[i];
     wmax = fmaxf(wmax, w32[i]);
   }
   uint32_t q = 0;
@@ -840,13 +851,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
             const float2 sg = make_float2(sign_one(vv.x), sign_one(vv.y));
             // t = k * sign(vote) + 0 (exact; +0 for k = 0): t < 0 <=> entry opposes the majority.
             // Erased entries are counted from t's sign bit on the FMA pipe, survivors kept as max(t, 0).
+            // survivors: w * max(t, 0) == (w / 2) * (t + |t|) exactly (both steps are power-of-two scalings)
             float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int i = 0; i < N; ++i) {
               const float2 t2 = __ffma2_rn(k2[i], sg, make_float2(0.f, 0.f));
-              cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i]);
-              cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i]);
-              acc = __ffma2_rn(make_float2(w32[i], w32[i]), make_float2(fmaxf(t2.x, 0.f), fmaxf(t2.y, 0.f)), acc);
+              cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i], a.two);
+              cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i], a.two);
+              const float2 tp = __fadd2_rn(t2, make_float2(fabsf(t2.x), fabsf(t2.y)));
+              acc = __ffma2_rn(make_float2(wh32[i], wh32[i]), tp, acc);
             }
             y2 = __ffma2_rn(sg, acc, b2);
           } else {
@@ -1150,6 +1163,7 @@ int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, i
   a.erase_mode = erase_mode;
   a.delta_mode = delta_mode & 1;
   a.with_base = (delta_mode & 1) ? ((delta_mode >> 1) & 1) : 1;
+  a.two = 2;
   const char* env = getenv("RLK_MERGE_FAST");
   a.fast = env ? atoi(env) : 1;
   cudaStream_t s = (cudaStream_t)stream;

@@ -13,7 +13,10 @@ constexpr int kThreads = kCThreads + 32;
 __device__ __forceinline__ void cbar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kCThreads) : "memory"); }
 
 // K3 fast path consumer warps (8: more forces <= 128 registers and spills)
-constexpr int kFastCWarps = 16;
+#ifndef RLK_FAST_CWARPS
+#define RLK_FAST_CWARPS 16
+#endif
+constexpr int kFastCWarps = RLK_FAST_CWARPS;
 constexpr int kFastCThreads = kFastCWarps * 32;
 constexpr int kFastThreads = kFastCThreads + 32;
 
