@@ -694,6 +694,18 @@ __device__ __forceinline__ uint32_t add_sign_bit(uint32_t x, uint32_t c, uint32_
   (void)two;
   return r;
 }
+// PRMT in sign-replicate mode: each result byte = 0x00 / 0xFF from the sign bit of the selected byte
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t x, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(x), "r"(sel));
+  return r;
+}
+// (x & m) | (b & ~m) in one LOP3
+__device__ __forceinline__ uint32_t select_halves(uint32_t x, uint32_t b, uint32_t m) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xe4;" : "=r"(r) : "r"(x), "r"(b), "r"(m));
+  return r;
+}
 // +-1.0f with the sign of x (one LOP3)
 __device__ __forceinline__ float sign_one(float x) {
   uint32_t r;
@@ -804,8 +816,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
           xw4[i] = FastVec::load(sb + (i + 1) * SB + v * (2 * kFastElems));
           kb[i] = DROP ? ((uint32_t)bm[i * BMB + (le >> 3)] >> (le & 7)) : 0xffu;
         }
+        // dropout on the integer side: the thread's 4 keep bits go to byte sign bits (one IMAD), PRMT
+        // sign-replication turns them into halfword masks, and one LOP3 per word swaps every dropped
+        // expert half for the base half, so d = x - b is exactly +0 there (reference: k = 0, fusion.py:114)
+        static_assert(kFastPairs == 2, "the keep-bit spread assumes 4 elements per thread-vector");
+        uint32_t spread[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) spread[i] = DROP ? (((kb[i] & 0xfu) * 0x10204080u) & 0x80808080u) : 0u;
         uint32_t outw[kFastPairs];
-        uint32_t slowm = 0;
+        float gm[kFastElems];  // signed guard margin per element: < 0 -> recompute exactly
 #pragma unroll
         for (int p = 0; p < kFastPairs; ++p) {
           const uint32_t bw = bw4.w[p];
@@ -814,19 +833,13 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
           float2 aa = make_float2(0.f, 0.f);
 #pragma unroll
           for (int i = 0; i < N; ++i) {
-            const uint32_t xw = xw4[i].w[p];
+            uint32_t xw = xw4[i].w[p];
+            if (DROP) xw = select_halves(xw, bw, prmt_sign(spread[i], p == 0 ? 0x9988u : 0xBBAAu));
             const float2 d2 = __ffma2_rn(b2, make_float2(-1.f, -1.f), make_float2(bf16_lo(xw), bf16_hi(xw)));
-            if (DROP) {
-              const float2 m2 = make_float2(((kb[i] >> (2 * p)) & 1u) ? sr32[i] : 0.f,
-                                            ((kb[i] >> (2 * p + 1)) & 1u) ? sr32[i] : 0.f);
-              k2[i] = __fmul2_rn(d2, m2);
-            } else {
-              k2[i] = __fmul2_rn(d2, make_float2(sr32[i], sr32[i]));
-            }
+            k2[i] = __fmul2_rn(d2, make_float2(sr32[i], sr32[i]));
             aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
           }
-          bool sl = false, sh = false;
-          float2 y2;
+          float2 y2, g1 = make_float2(1.f, 1.f);
           if constexpr (kErase) {
             float2 vv, gg;
             if (ERASE == 1) {
@@ -843,15 +856,13 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
                 gg = __ffma2_rn(k2[i], k2[i], gg);
               }
             }
-            // |vote| must clear the certified error bound; an all-zero column (vote = bound = 0) is an
-            // exact tie and needs no fallback
-            const float2 cg = __fmul2_rn(make_float2(cv, cv), gg);
-            sl = !(fabsf(vv.x) >= cg.x);
-            sh = !(fabsf(vv.y) >= cg.y);
+            // |vote| - c * bound (one rounding: its sign is exact).  < 0: the f32 vote's sign is not
+            // certain; an all-zero column gives 0 - 0 = 0 (an exact tie, no fallback needed)
+            g1 = __ffma2_rn(make_float2(-cv, -cv), gg, make_float2(fabsf(vv.x), fabsf(vv.y)));
             const float2 sg = make_float2(sign_one(vv.x), sign_one(vv.y));
             // t = k * sign(vote) + 0 (exact; +0 for k = 0): t < 0 <=> entry opposes the majority.
-            // Erased entries are counted from t's sign bit on the FMA pipe, survivors kept as max(t, 0).
-            // survivors: w * max(t, 0) == (w / 2) * (t + |t|) exactly (both steps are power-of-two scalings)
+            // Erased entries are counted from t's sign bit; survivors enter as
+            // w * max(t, 0) == (w / 2) * (t + |t|) exactly (both steps are power-of-two scalings)
             float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int i = 0; i < N; ++i) {
@@ -867,16 +878,23 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
 #pragma unroll
             for (int i = 0; i < N; ++i) y2 = __ffma2_rn(make_float2(w32[i], w32[i]), k2[i], y2);
           }
-          // bf16 rounding must be certain: distance to the rounding midpoint > error bound
+          // bf16 rounding must be certain: |y - midpoint| - 2^-19 * (|b| + max w * sum|k|) >= 0
           const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, make_float2(fabsf(b2.x), fabsf(b2.y)));
           const float2 mid = make_float2(mid_of(y2.x), mid_of(y2.y));
           const float2 dm = __fadd2_rn(y2, make_float2(-mid.x, -mid.y));
-          const float2 eb = __fmul2_rn(make_float2(0x1p-19f, 0x1p-19f), S2);
-          sl = sl || !(fabsf(dm.x) > eb.x);
-          sh = sh || !(fabsf(dm.y) > eb.y);
-          slowm |= ((uint32_t)sl | ((uint32_t)sh << 1)) << (2 * p);
+          const float2 g2 = __ffma2_rn(make_float2(-0x1p-19f, -0x1p-19f), S2, make_float2(fabsf(dm.x), fabsf(dm.y)));
+          gm[2 * p] = fminf(g1.x, g2.x);
+          gm[2 * p + 1] = fminf(g1.y, g2.y);
           __nv_bfloat162 p2 = __floats2bfloat162_rn(y2.x, y2.y);
           outw[p] = *reinterpret_cast<uint32_t*>(&p2);
+        }
+        float gmin = gm[0];
+#pragma unroll
+        for (int e = 1; e < kFastElems; ++e) gmin = fminf(gmin, gm[e]);
+        uint32_t slowm = 0;
+        if (gmin < 0.f) {
+#pragma unroll
+          for (int e = 0; e < kFastElems; ++e) slowm |= (uint32_t)(gm[e] < 0.f) << e;
         }
         if (slowm) {  // phase 2 (rare): exact reference-order evaluation of flagged elements
 #pragma unroll
