@@ -219,8 +219,12 @@ def fusion_bench(args, rank, world, local, group):
 
 
 def fusion_e2e(args, pieces, call, weights, stream, dev, group):
-    """H2D base + experts from pinned host memory, fuse, D2H the fused output -- every step."""
+    """End to end through the public API from pinned host memory, every step: H2D of base + experts,
+    fusion, D2H of the fused output.  At N = 1 the state dict is processed in tensor groups on three
+    streams -- H2D of group g+1, K2/K1/finalize/K3 of group g and D2H of group g-1 overlap (per-tensor
+    norms only need the tensor's own data).  At N > 1 the sharded step runs after a full H2D."""
     import torch
+    from paper_2509_18883_b200 import fusion as F
     total = sum(p.numel for p in pieces)
     dt = pieces[0].base.dtype
     host_in = [torch.empty(total, dtype=dt, pin_memory=True) for _ in range(N_EXPERTS + 1)]
@@ -236,15 +240,58 @@ def fusion_e2e(args, pieces, call, weights, stream, dev, group):
             for h, d in zip(hv, [p.base, *p.experts]):
                 h.copy_(d, non_blocking=True)
     stream.synchronize()
+    world = 1 if group is None else torch.distributed.get_world_size(group)
+    pipelined = world == 1
+    if pipelined:
+        # consecutive tensor groups of ~2 GB of inputs; one FusionCall (plan) per group
+        groups, cur, cur_b = [], [], 0
+        for v in views:
+            cur.append(v)
+            cur_b += v[0].numel * 2 * (N_EXPERTS + 1)
+            if cur_b >= (2 << 30):
+                groups.append(cur)
+                cur, cur_b = [], 0
+        if cur:
+            groups.append(cur)
+        h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        calls = []
+        for gv in groups:
+            gp = [F.Piece(k, 0, v[0].base, v[0].experts, v[0].out) for k, v in enumerate(gv)]
+            calls.append(F.FusionCall(gp, F.FusionLayout([v[0].numel for v in gv]), N_EXPERTS, call.cfg, stream=stream))
 
     def step():
-        with torch.cuda.stream(stream):
-            for p, hv, _ in views:
-                for h, d in zip(hv, [p.base, *p.experts]):
-                    d.copy_(h, non_blocking=True)
-            call.run(weights)
-            for p, _, ho in views:
-                ho.copy_(p.out, non_blocking=True)
+        if not pipelined:
+            with torch.cuda.stream(stream):
+                for p, hv, _ in views:
+                    for h, d in zip(hv, [p.base, *p.experts]):
+                        d.copy_(h, non_blocking=True)
+                call.run(weights)
+                for p, _, ho in views:
+                    ho.copy_(p.out, non_blocking=True)
+            return
+        # the compute stream is the one the timing events are recorded on: make it wait for the tail
+        start = torch.cuda.Event()
+        start.record(stream)
+        h2d_s.wait_event(start)
+        d2h_s.wait_event(start)
+        for gv, c in zip(groups, calls):
+            with torch.cuda.stream(h2d_s):
+                for p, hv, _ in gv:
+                    for h, d in zip(hv, [p.base, *p.experts]):
+                        d.copy_(h, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(h2d_s)
+            stream.wait_event(ready)
+            c.run(weights)
+            done = torch.cuda.Event()
+            done.record(stream)
+            d2h_s.wait_event(done)
+            with torch.cuda.stream(d2h_s):
+                for p, _, ho in gv:
+                    ho.copy_(p.out, non_blocking=True)
+        end = torch.cuda.Event()
+        end.record(d2h_s)
+        stream.wait_event(end)
 
     steps, warm = max(1, min(args.steps, args.e2e_steps)), 1
     for _ in range(warm):
@@ -261,7 +308,9 @@ def fusion_e2e(args, pieces, call, weights, stream, dev, group):
     ms, = max_over_ranks([e0.elapsed_time(e1) / steps], group)
     h2d, d2h = sum_over_ranks([float(total * 2 * (N_EXPERTS + 1)), float(total * 2)], group)
     del host_in, host_out, views
-    return dict(e2e_ms=ms, e2e_steps=steps, e2e_warmup=warm, h2d=int(h2d), d2h=int(d2h))
+    return dict(e2e_ms=ms, e2e_steps=steps, e2e_warmup=warm, h2d=int(h2d), d2h=int(d2h),
+                e2e_path=("pipelined tensor groups (H2D | fuse | D2H on 3 streams)" if pipelined
+                          else "sharded: H2D, fuse with NCCL norm all_reduce, D2H"))
 
 
 # ----------------------------------------------------------------------------------- GRPO
@@ -480,7 +529,7 @@ def main():
                        "h2d_bytes_per_step": fz["h2d"], "d2h_bytes_per_step": fz["d2h"],
                        "ms_per_step": fz["e2e_ms"], "steps": fz["e2e_steps"], "warmup": fz["e2e_warmup"],
                        "h2d_gbs": fz["h2d"] / (fz["e2e_ms"] / 1e3) / 1e9,
-                       "path": "fusion.FusionCall over pinned host buffers (H2D inputs, K1..K3, D2H output)"}
+                       "path": fz["e2e_path"]}
     if gr is not None:
         tok = gr["tokens"]
         fwd_b = gr["kern"]["rlk_grpo_fwd"]
