@@ -58,7 +58,7 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
   constexpr uint32_t BMB = ELEMS / 8;  // bitmap bytes per expert per full stage
   const int ns = with_base ? N + 1 : N;
   const uint64_t pol = policy_evict_first();
-  uint32_t q = 0;
+  RingPos q;
   for (uint32_t item = blockIdx.x; item < plan.n_items; item += gridDim.x) {
     const ItemGeom g = item_geom(plan, item);
     const char* src[N + 1];
@@ -75,7 +75,7 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_bytes = (n * ESZ) & ~15u;
       const uint32_t bm_bytes = bitmap ? (((n + 7) / 8 + 15) & ~15u) : 0u;
-      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.empty[s], ph ^ 1u);
       const uint32_t tx = main_bytes * ns + bm_bytes * N;
       uint8_t* dst = r.buf + s * r.stage_bytes;
@@ -94,7 +94,7 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
       } else {
         mbar_arrive(&r.full[s]);
       }
-      ++q;
+      q.next(r.nstages);
     }
   }
 }
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ S
   }
   __shared__ double red[kCWarps][N];
   const int tid = threadIdx.x;
-  uint32_t q = 0;
+  RingPos q;
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
     const ItemGeom g = item_geom(a.plan, item);
     const uint64_t jtensor0 = g.seg->j0 + g.start;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ S
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_elems = ((n * ESZ) & ~15u) / ESZ;
-      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.full[s], ph);
       const uint8_t* sb = r.buf + s * r.stage_bytes;
       const uint8_t* bm = sb + (N + 1) * SB;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ S
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[s]);
-      ++q;
+      q.next(r.nstages);
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq_bf16(const __grid_constan
   }
   __shared__ double red[kCWarps][N];
   const int tid = threadIdx.x;
-  uint32_t q = 0;
+  RingPos q;
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
     const ItemGeom g = item_geom(a.plan, item);
     const uint64_t jtensor0 = g.seg->j0 + g.start;
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq_bf16(const __grid_constan
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_elems = ((n * 2) & ~15u) / 2;
-      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.full[s], ph);
       const uint8_t* sb = r.buf + s * r.stage_bytes;
       const uint8_t* bm = sb + (N + 1) * SB;
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq_bf16(const __grid_constan
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[s]);
-      ++q;
+      q.next(r.nstages);
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
     return;
   }
   const int tid = threadIdx.x;
-  uint32_t q = 0;
+  RingPos q;
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
     const ItemGeom g = item_geom(a.plan, item);
     const double* scale = a.scale + (uint64_t)g.tensor * N;
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_elems = ((n * ESZ) & ~15u) / ESZ;
-      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.full[s], ph);
       const uint8_t* sb = r.buf + s * r.stage_bytes;
       const uint8_t* bm = sb + (N + 1) * SB;
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ M
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[s]);
-      ++q;
+      q.next(r.nstages);
     }
     // per-item counters -> per-tensor u64 totals (integer atomics: order-independent)
 #pragma unroll
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
     wh32[i] = 0.5f * w32[i];
     wmax = fmaxf(wmax, w32[i]);
   }
-  uint32_t q = 0;
+  RingPos q;
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
     const ItemGeom g = item_geom(a.plan, item);
     const double* scale = a.scale + (uint64_t)g.tensor * N;
@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_elems = ((n * 2) & ~15u) / 2;
-      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.full[s], ph);
       const uint8_t* sb = r.buf + s * r.stage_bytes;
       const uint8_t* bm = sb + (N + 1) * SB;
@@ -820,6 +820,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
         // sign-replication turns them into halfword masks, and one LOP3 per word swaps every dropped
         // expert half for the base half, so d = x - b is exactly +0 there (reference: k = 0, fusion.py:114)
         static_assert(kFastPairs == 2, "the keep-bit spread assumes 4 elements per thread-vector");
+  static_assert(N <= 8, "output guard certified for N <= 11");
         uint32_t spread[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) spread[i] = DROP ? (((kb[i] & 0xfu) * 0x10204080u) & 0x80808080u) : 0u;
@@ -878,11 +879,13 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
 #pragma unroll
             for (int i = 0; i < N; ++i) y2 = __ffma2_rn(make_float2(w32[i], w32[i]), k2[i], y2);
           }
-          // bf16 rounding must be certain: |y - midpoint| - 2^-19 * (|b| + max w * sum|k|) >= 0
+          // bf16 rounding must be certain: |y - midpoint| - 2^-20 * (|b| + max w * sum|k|) >= 0.  The f32
+          // evaluation error is <= (4 + N + 1) * 2^-24 * (|b| + max w * sum|k|): 3 roundings in k, 1 in w,
+          // N in the weighted sum, 1 in y -- so 2^-20 = 16 * 2^-24 is certified for N <= 11.
           const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, make_float2(fabsf(b2.x), fabsf(b2.y)));
           const float2 mid = make_float2(mid_of(y2.x), mid_of(y2.y));
           const float2 dm = __fadd2_rn(y2, make_float2(-mid.x, -mid.y));
-          const float2 g2 = __ffma2_rn(make_float2(-0x1p-19f, -0x1p-19f), S2, make_float2(fabsf(dm.x), fabsf(dm.y)));
+          const float2 g2 = __ffma2_rn(make_float2(-0x1p-20f, -0x1p-20f), S2, make_float2(fabsf(dm.x), fabsf(dm.y)));
           gm[2 * p] = fminf(g1.x, g2.x);
           gm[2 * p + 1] = fminf(g1.y, g2.y);
           __nv_bfloat162 p2 = __floats2bfloat162_rn(y2.x, y2.y);
@@ -948,7 +951,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[s]);
-      ++q;
+      q.next(r.nstages);
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {

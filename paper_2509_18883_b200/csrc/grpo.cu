@@ -61,14 +61,14 @@ template <> struct RowVec<RLK_F64> {
 template <typename Active, typename Addr>
 __device__ void produce_rows(const Ring& r, uint64_t n_rows, uint64_t row_bytes, Active active, Addr addr) {
   const uint64_t pol = policy_evict_first();
-  uint32_t q = 0;
+  RingPos q;
   for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
     if (!active(row)) continue;
     const char* src = addr(row);
     for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
       const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
       const uint32_t main_bytes = bytes & ~15u;
-      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.empty[s], ph ^ 1u);
       if (main_bytes) {
         mbar_arrive_expect_tx(&r.full[s], main_bytes);
@@ -76,7 +76,7 @@ __device__ void produce_rows(const Ring& r, uint64_t n_rows, uint64_t row_bytes,
       } else {
         mbar_arrive(&r.full[s]);
       }
-      ++q;
+      q.next(r.nstages);
     }
   }
 }
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd(FwdArgs a) {
     return;
   }
   __shared__ double red_m[kGW], red_s[kGW];
-  uint32_t q = 0;
+  RingPos q;
   for (uint64_t row = blockIdx.x; row < a.n_rows; row += gridDim.x) {
     if (!active(row)) {
       if (tid == 0) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd(FwdArgs a) {
       for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
         const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
         const uint32_t main_bytes = bytes & ~15u;
-        const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+        const uint32_t s = q.s, ph = q.ph;
         mbar_wait(&r.full[s], ph);
         const uint8_t* sb = r.buf + s * r.stage_bytes;
         for (uint32_t v = tid; v < main_bytes / 16; v += kGT) {
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd(FwdArgs a) {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&r.empty[s]);
-        ++q;
+        q.next(r.nstages);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd(FwdArgs a) {
       for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
         const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
         const uint32_t main_bytes = bytes & ~15u;
-        const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+        const uint32_t s = q.s, ph = q.ph;
         mbar_wait(&r.full[s], ph);
         const uint8_t* sb = r.buf + s * r.stage_bytes;
         const uint32_t nvec = main_bytes / 16;
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd(FwdArgs a) {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&r.empty[s]);
-        ++q;
+        q.next(r.nstages);
       }
       sum += sum2;
 #pragma unroll
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd_stream(FwdArgs a, flo
     if (lane == 0) produce_rows(r, a.n_rows, row_bytes, streamed, addr);
     return;
   }
-  uint32_t q = 0;
+  RingPos q;
   for (uint64_t row = blockIdx.x; row < a.n_rows; row += gridDim.x) {
     if (!active(row)) continue;
     const char* rowp = addr(row);
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd_stream(FwdArgs a, flo
       for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
         const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
         const uint32_t main_bytes = bytes & ~15u;
-        const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+        const uint32_t s = q.s, ph = q.ph;
         mbar_wait(&r.full[s], ph);
         const uint8_t* sb = r.buf + s * r.stage_bytes;
         const uint32_t nvec = main_bytes / 16;
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd_stream(FwdArgs a, flo
           take((float)load_f64<DT>(rowp, off / ESZ + e));
         __syncwarp();
         if (lane == 0) mbar_arrive(&r.empty[s]);
-        ++q;
+        q.next(r.nstages);
       }
     }
     sum += sum2;
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_bwd(BwdArgs a) {
     if (lane == 0) produce_rows(r, a.n_out_rows, row_bytes, streamed, addr);
     return;
   }
-  uint32_t q = 0;
+  RingPos q;
   for (uint64_t o = blockIdx.x; o < a.n_out_rows; o += gridDim.x) {
     char* grow = a.grad + lrow(o) * a.grad_row_stride * GSZ;
     if (!active(o)) {
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_bwd(BwdArgs a) {
     for (uint64_t off = 0; off < row_bytes; off += r.stage_bytes) {
       const uint32_t bytes = (uint32_t)umin64((uint64_t)r.stage_bytes, row_bytes - off);
       const uint32_t main_bytes = bytes & ~15u;
-      const uint32_t s = q % r.nstages, ph = (q / r.nstages) & 1u;
+      const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.full[s], ph);
       const uint8_t* sb = r.buf + s * r.stage_bytes;
       const uint64_t v0 = off / ESZ;  // first vocab index of this stage
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_bwd(BwdArgs a) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[s]);
-      ++q;
+      q.next(r.nstages);
     }
   }
 }

@@ -20,6 +20,17 @@ constexpr int kFastCWarps = RLK_FAST_CWARPS;
 constexpr int kFastCThreads = kFastCWarps * 32;
 constexpr int kFastThreads = kFastCThreads + 32;
 
+// Position in the ring: slot and the mbarrier phase parity of the current lap (no runtime division).
+struct RingPos {
+  uint32_t s = 0, ph = 0;
+  __device__ __forceinline__ void next(uint32_t n) {
+    if (++s == n) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
 struct Ring {
   uint8_t* buf;
   uint64_t* full;
