@@ -50,10 +50,9 @@ __device__ __forceinline__ ItemGeom item_geom(const rlk_fusion_plan& plan, uint3
 
 // Producer: one elected lane streams every (item, stage) of this CTA through the ring.
 // Stage layout: [stream 0 | stream 1 | ... | stream NS-1 | bitmap expert 0 | ... | bitmap expert N-1].
-template <int ESZ, int N>
+template <int ESZ, int N, uint32_t SB = StreamBytes<N>::v>
 __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_base, const uint32_t* bitmap,
                         uint64_t words_per_row) {
-  constexpr uint32_t SB = StreamBytes<N>::v;
   constexpr uint32_t ELEMS = SB / ESZ;
   constexpr uint32_t BMB = ELEMS / 8;  // bitmap bytes per expert per full stage
   const int ns = with_base ? N + 1 : N;
@@ -727,6 +726,10 @@ __device__ __forceinline__ float mid_of(float y) {
 #define RLK_FAST_PAIRS 2
 #endif
 constexpr int kFastPairs = RLK_FAST_PAIRS;
+#ifndef RLK_FAST_SB
+#define RLK_FAST_SB 16384
+#endif
+constexpr uint32_t kFastSB = RLK_FAST_SB;  // bytes per stream per stage in the fast merge
 constexpr int kFastElems = 2 * kFastPairs;
 struct FastVec {
   uint32_t w[kFastPairs];
@@ -758,14 +761,14 @@ struct FastVec {
 template <int N, int DROP, int ERASE>
 __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_constant__ MergeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr uint32_t SB = StreamBytes<N>::v;
+  constexpr uint32_t SB = kFastSB;
   constexpr uint32_t ELEMS = SB / 2;
   constexpr uint32_t BMB = ELEMS / 8;
   constexpr bool kErase = (ERASE != 0) && (N >= 2);
   const Ring r = ring_setup(smem, a.stage_bytes, a.nstages, kFastCWarps);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kFastCWarps) {
-    if (lane == 0) produce<2, N>(a.plan, r, true, DROP == 2 ? a.bitmap : nullptr, a.words_per_row);
+    if (lane == 0) produce<2, N, kFastSB>(a.plan, r, true, DROP == 2 ? a.bitmap : nullptr, a.words_per_row);
     return;
   }
   const int tid = threadIdx.x;
@@ -1002,6 +1005,10 @@ static int launch_sumsq(SumsqArgs& a, cudaStream_t s) {
 
 template <int N, int DROP, int ERASE>
 static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
+  uint32_t sb = (N + 1) * kFastSB + (DROP ? N * (kFastSB / 2 / 8) : 0);
+  sb = (sb + 127) & ~127u;
+  a.stage_bytes = sb;
+  a.nstages = std::min<uint32_t>(8, (kSmemBudget - 1024) / sb);
   const uint32_t smem = 1024 + a.stage_bytes * a.nstages;
   auto kern = k_merge_fast<N, DROP, ERASE>;
   int st = ensure_smem(kern, smem);
