@@ -165,6 +165,12 @@ int rlk_scaled_add(const void* a, const void* b, double alpha, void* out, int dt
 int rlk_synth_normal(void* out, int dtype, uint64_t n, uint64_t j0, uint64_t seed, double std_dev,
                      const void* base, void* stream);
 
+/* Checkpoint checksum ("flat LE f64 + checksum"): *out += sum_i mix64(w_i ^ ((word_offset + i + 1)
+ * * 0x9E3779B97F4A7C15)) mod 2^64 over n_words 64-bit words (8-byte aligned).  Chunks may be summed in
+ * any order.  out is a device u64 (caller zeroes). */
+int rlk_checksum64(const void* data, uint64_t n_words, uint64_t word_offset, unsigned long long* out,
+                   void* stream);
+
 /* ---- K7 host streaming loader (checkpoints larger than HBM) -------------------------------------
  * A ring of n_slots pinned host slots of slot_bytes each and n_threads host workers (0 = all cores).
  * h2d / d2h pipeline pageable<->pinned memcpy against cudaMemcpyAsync on `stream`; the device side of

@@ -63,6 +63,7 @@ SIGNATURES = {
     "rlk_nonfinite_count": (_I, [_P, _I, _U64, _P, _P]),
     "rlk_scaled_add": (_I, [_P, _P, _D, _P, _I, _U64, _P]),
     "rlk_synth_normal": (_I, [_P, _I, _U64, _U64, _U64, _D, _P, _P]),
+    "rlk_checksum64": (_I, [_P, _U64, _U64, _P, _P]),
     "rlk_loader_create": (_P, [_U64, _I, _I]),
     "rlk_loader_destroy": (None, [_P]),
     "rlk_loader_last_error": (C.c_char_p, []),

@@ -139,3 +139,29 @@ extern "C" int rlk_synth_normal(void* out, int dtype, uint64_t n, uint64_t j0, u
   }
   return launch_status("rlk_synth_normal");
 }
+
+// ---------------------------------------------------------------------------------------------
+// Checkpoint checksum (checkpoint.py): sum over 64-bit words w_i at global word index o + i of
+// mix64(w_i ^ ((o + i + 1) * GAMMA)) mod 2^64.  Position-keyed (detects permutations) and a plain
+// modular sum (so chunks can be checksummed independently and added, in any order).
+namespace rlk {
+__global__ void k_checksum64(const uint64_t* __restrict__ w, uint64_t n, uint64_t off, unsigned long long* out) {
+  uint64_t acc = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    acc += mix64(w[i] ^ ((off + i + 1) * kGamma));
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, (unsigned long long)acc);
+}
+}  // namespace rlk
+
+extern "C" int rlk_checksum64(const void* data, uint64_t n_words, uint64_t word_offset, unsigned long long* out,
+                              void* stream) {
+  RLK_REQUIRE(out != nullptr, "rlk_checksum64: out is NULL");
+  if (n_words == 0) return RLK_OK;
+  RLK_REQUIRE(data != nullptr && ((uintptr_t)data & 7u) == 0, "rlk_checksum64: data must be 8-byte aligned");
+  const uint64_t blocks = (n_words + 255) / 256;
+  const int grid = (int)(blocks < (uint64_t)sm_count() * 8 ? blocks : (uint64_t)sm_count() * 8);
+  k_checksum64<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint64_t*)data, n_words, word_offset, out);
+  return launch_status("rlk_checksum64");
+}
