@@ -337,34 +337,23 @@ def grpo_bench(args, rank, world, local, group):
     adv = np.where(np.arange(chunk) % 2 == 0, 1.0, -1.0)
     batch = O.GRPOBatch.pack(toks, lt, li, np.arange(chunk + 1) * T, adv, np.ones(chunk, np.uint8), chunk, T,
                              device=dev)
-    grad = torch.empty_like(logits)
     n_chunks = (len(mine) + chunk - 1) // chunk
     torch.cuda.synchronize(dev)
 
     def run(bwd: bool, events=None):
         for _ in range(n_chunks):
+            a = b = None
             if events is not None:
                 a = torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-            fwd = O.grpo_forward(logits, batch, stream=stream)
+            if bwd:  # loss + gradient in one read of the logits (rlk_grpo_fused_bf16, 2-CTA clusters)
+                O.grpo_forward_backward(logits, batch, stream=stream)
+            else:
+                O.grpo_forward(logits, batch, stream=stream)
             if events is not None:
                 b = torch.cuda.Event(enable_timing=True)
                 b.record(stream)
-                events.setdefault("rlk_grpo_fwd", []).append((a, b))
-            if bwd:
-                with torch.cuda.stream(stream):
-                    coef = fwd.coef
-                    temp_tok = batch.temperature[batch.sample_of_row.long()]
-                    c = torch.cuda.Event(enable_timing=True) if events is not None else None
-                    if c is not None:
-                        c.record(stream)
-                    L.call("rlk_grpo_bwd", L.ptr(logits), L.RLK_BF16, rows, V, V, None, None, None,
-                           L.ptr(batch.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(coef), L.ptr(grad),
-                           L.RLK_BF16, V, L.stream_handle(stream))
-                    if c is not None:
-                        d = torch.cuda.Event(enable_timing=True)
-                        d.record(stream)
-                        events.setdefault("rlk_grpo_bwd", []).append((c, d))
+                events.setdefault("rlk_grpo_fused_bf16" if bwd else "rlk_grpo_fwd", []).append((a, b))
 
     out = {}
     for bwd in (False, True):
@@ -382,12 +371,13 @@ def grpo_bench(args, rank, world, local, group):
         ms, = max_over_ranks([e0.elapsed_time(e1) / args.steps], group)
         out["fwdbwd_ms" if bwd else "fwd_ms"] = ms
     ev = {}
+    run(False, ev)
     run(True, ev)
     torch.cuda.synchronize(dev)
     kern = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
     kmax = dict(zip(kern, max_over_ranks(list(kern.values()), group)))
     out.update(kern=kmax, rows_per_launch=rows, tokens=G * T, V=V)
-    del logits, grad
+    del logits
     torch.cuda.empty_cache()
     return out
 
@@ -537,6 +527,10 @@ def main():
         line["grpo"] = {"workload": f"config5: V={gr['V']}, G=16 x T={tok // 16} tokens (one group), bf16 logits",
                         "tokens_per_s": tok / (gr["fwd_ms"] / 1e3), "fwd_ms": gr["fwd_ms"],
                         "fwd_bwd_tokens_per_s": tok / (gr["fwdbwd_ms"] / 1e3), "fwd_bwd_ms": gr["fwdbwd_ms"],
+                        "fwd_bwd_path": "rlk_grpo_fused_bf16 (one read of the logits, bf16 grad written)",
+                        "fwd_bwd_roofline": {"achieved": gr["rows_per_launch"] * gr["V"] * 4 / (gr["kern"]["rlk_grpo_fused_bf16"] / 1e3) / 1e9,
+                                             "peak": peak, "unit": "GB/s", "bytes_per_token": gr["V"] * 4,
+                                             "frac": gr["rows_per_launch"] * gr["V"] * 4 / (gr["kern"]["rlk_grpo_fused_bf16"] / 1e3) / 1e9 / peak},
                         "roofline": {"bound": "hbm", "kernel": "rlk_grpo_fwd", "achieved": ach, "peak": peak,
                                      "unit": "GB/s", "frac": ach / peak, "bytes_per_token": gr["V"] * 2 + 12},
                         "kernels_ms": gr["kern"]}

@@ -17,7 +17,7 @@ INCLUDE = PKG.parent / "include"
 LIB = PKG / "_rlk.so"
 BUILD = PKG.parent / "build"
 
-CU_SOURCES = ["capi.cu", "fusion.cu", "grpo.cu"]
+CU_SOURCES = ["capi.cu", "fusion.cu", "grpo.cu", "grpo_fused.cu"]
 CPP_SOURCES = ["loader.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

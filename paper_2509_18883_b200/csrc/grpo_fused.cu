@@ -1,0 +1,368 @@
+// Fused single-pass GRPO forward + backward for bf16 logits (K4+K5 in one read of the logits).
+//
+// objective_value and objective_gradient (pkg/src/rolloutlab/objective.py:230-283) both need the
+// row's log-sum-exp; the backward additionally needs coef = norm * w * slope * r / T, known only after
+// the whole row was reduced.  A row (V = 131072 bf16 = 256 KiB) does not fit one SM's shared memory,
+// so a 2-CTA thread-block cluster owns it: each CTA streams its half into shared memory (TMA bulk
+// copies, 16 KiB chunks, one mbarrier per chunk), reduces it (online max / sum of 2^(z c - m c)),
+// and sends its (max, sum) partial into the peer CTA's shared memory with st.async, which completes
+// a transaction on the peer's mbarrier -- no cluster-wide barrier per row.  Both CTAs then run the
+// same f64 epilogue, write coef * (onehot - softmax) for their half from shared memory, and release
+// each chunk to the producer, which is already streaming the next row in.  Logits are read once:
+// 4 bytes of HBM traffic per logit for loss + gradient instead of 6 (K4 then K5).
+#include "common.cuh"
+#include "capi_internal.h"
+#include "pipeline.cuh"
+
+namespace rlk {
+
+constexpr int kFW = 16;                   // consumer warps
+constexpr int kFT = kFW * 32;
+constexpr int kFThreads = kFT + 32;       // + producer warp
+constexpr uint32_t kChunkBytes = 16384;   // TMA chunk (8192 bf16)
+constexpr uint32_t kMaxHalfBytes = 200 * 1024;
+constexpr double kLog2eF = 1.4426950408889634074;
+
+__device__ __forceinline__ void fbar_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kFT) : "memory"); }
+__device__ __forceinline__ float ex2f_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t n_clusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+// 8-byte store into the peer CTA's shared memory, completing 8 tx bytes on the peer's mbarrier
+__device__ __forceinline__ void st_async_peer(uint32_t remote_addr, float a, float b, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
+               "f"(a), "f"(b), "r"(remote_bar)
+               : "memory");
+}
+
+struct FusedArgs {
+  const char* logits;
+  uint64_t n_rows, vocab, row_stride;
+  const int64_t* row_index;
+  const int32_t* tokens;
+  const double *lp_train, *lp_infer;
+  const int32_t* sample;
+  const double* adv;
+  const uint8_t* use;
+  const double* temp;
+  const double* norm;
+  rlk_clip clip;
+  double grad_scale;
+  double *logp, *lse, *term, *coef;
+  int32_t* flags;
+  uint16_t* grad;
+  uint64_t grad_row_stride;
+  uint32_t nslots;
+};
+
+struct TripletF { double value, slope; };
+__device__ __forceinline__ TripletF triplet_f(double r, double adv, const rlk_clip& c) {  // objective.py:133-150
+  const double lo = 1.0 - c.eps_neg_low, hi = 1.0 + c.eps_pos_high;
+  const double clipped = fmin(fmax(r, lo), hi);
+  const double clip_slope = (lo <= r && r <= hi) ? 1.0 : 0.0;
+  const double raw = __dmul_rn(r, adv), capped = __dmul_rn(clipped, adv);
+  double inner, islope;
+  if (raw <= capped) { inner = raw; islope = adv; }
+  else { inner = capped; islope = __dmul_rn(adv, clip_slope); }
+  if (c.guard_positive && adv > 0.0) return {inner, islope};
+  const double floor_v = __dmul_rn(c.eps_neg_high, adv);
+  if (inner >= floor_v) return {inner, islope};
+  return {floor_v, 0.0};
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo_fused_bf16(FusedArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // layout: [full[nch] | empty[nch] | xbar[2] | pad] [slot[2] float2] [coef broadcast] ... 1 KiB header
+  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
+  const uint64_t half = a.vocab / 2;  // elements owned by this CTA (vocab % 16 == 0)
+  const uint64_t v0 = rank * half;
+  const uint32_t half_bytes = (uint32_t)(half * 2);
+  const uint32_t nch = (half_bytes + kChunkBytes - 1) / kChunkBytes;  // chunks per half row
+  const uint32_t nslots = a.nslots;  // ring slots >= nch: the producer runs ahead into the next row
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + nslots;
+  uint64_t* xbar = empty + nslots;
+  float2* slot = reinterpret_cast<float2*>(smem + 512);
+  float* bcast = reinterpret_cast<float*>(smem + 576);
+  float* red = reinterpret_cast<float*>(smem + 640);  // [kFW][2]
+  uint8_t* buf = smem + 1024;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < nslots; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], kFW);
+    }
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  cluster_sync_all();  // peers' barriers exist before any st.async targets them
+
+  auto active = [&](uint64_t row) { return a.use[a.sample[row]] != 0; };
+  auto row_ptr = [&](uint64_t row) {
+    const uint64_t rr = a.row_index ? (uint64_t)a.row_index[row] : row;
+    return a.logits + (rr * a.row_stride + v0) * 2;
+  };
+  const uint64_t row0 = cluster_id_x(), rstep = n_clusters_x();
+
+  if (warp == kFW) {
+    // ---------------- producer: chunk k of every active row into buffer slot k
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos q;
+      for (uint64_t row = row0; row < a.n_rows; row += rstep) {
+        if (!active(row)) continue;
+        const char* src = row_ptr(row);
+        for (uint32_t k = 0; k < nch; ++k) {
+          const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
+          mbar_wait(&empty[q.s], q.ph ^ 1u);
+          mbar_arrive_expect_tx(&full[q.s], bytes);
+          bulk_g2s(buf + q.s * kChunkBytes, src + (uint64_t)k * kChunkBytes, bytes, &full[q.s], pol);
+          q.next(nslots);
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers
+    RingPos q;
+    uint32_t xph[2] = {0u, 0u};
+    uint64_t it = 0;  // active rows seen: slot / exchange-barrier parity alternates strictly
+    for (uint64_t row = row0; row < a.n_rows; row += rstep) {
+      uint16_t* grow = a.grad + (a.row_index ? (uint64_t)a.row_index[row] : row) * a.grad_row_stride + v0;
+      if (!active(row)) {  // objective.py:240-241 / 275-276: no contribution, zero gradient
+        for (uint64_t b = (uint64_t)tid * 8; b < half; b += (uint64_t)kFT * 8)
+          stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
+        if (rank == 0 && tid == 0) {
+          if (a.logp) a.logp[row] = 0.0;
+          if (a.lse) a.lse[row] = 0.0;
+          a.term[row] = 0.0;
+          a.coef[row] = 0.0;
+        }
+        continue;
+      }
+      const uint32_t p = (uint32_t)(it++ & 1u);
+      const int32_t s_id = a.sample[row];
+      const double T = a.temp[s_id];
+      const float c = (float)(kLog2eF / T);
+      // epilogue operands are fetched now, so their latency hides behind pass 1
+      int32_t pf_tok = 0;
+      double pf_z = 0.0, pf_lt = 0.0, pf_li = 0.0, pf_adv = 0.0, pf_norm = 0.0;
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&xbar[p], 8);  // the peer's partial lands in slot[p]
+        pf_tok = a.tokens[row];
+        pf_lt = a.lp_train[row];
+        pf_li = a.lp_infer[row];
+        pf_adv = a.adv[s_id];
+        pf_norm = a.norm[s_id];
+        if (pf_tok >= 0 && (uint64_t)pf_tok < a.vocab)
+          pf_z = load_f64<RLK_BF16>(a.logits + (a.row_index ? (uint64_t)a.row_index[row] : row) * a.row_stride * 2,
+                                    (uint64_t)pf_tok);
+      }
+      // pass 1: online max / sum over this half
+      float mz = -INFINITY, s0 = 0.f, s1 = 0.f, nb = INFINITY;
+      const RingPos q_row = q;
+      for (uint32_t k = 0; k < nch; ++k) {
+        mbar_wait(&full[q.s], q.ph);
+        const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
+        const uint8_t* cb = buf + q.s * kChunkBytes;
+        q.next(nslots);
+        for (uint32_t v = tid; v < bytes / 16; v += kFT) {
+          const uint4 w = lds128(cb + v * 16);
+          float z[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
+                        bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
+          const float lm = fmaxf(fmaxf(fmaxf(z[0], z[1]), fmaxf(z[2], z[3])), fmaxf(fmaxf(z[4], z[5]), fmaxf(z[6], z[7])));
+          if (lm > mz) {
+            const float f = ex2f_approx((mz - lm) * c);
+            s0 *= f;
+            s1 *= f;
+            mz = lm;
+            nb = -mz * c;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            s0 += ex2f_approx(fmaf(z[e], c, nb));
+            s1 += ex2f_approx(fmaf(z[e + 1], c, nb));
+          }
+        }
+      }
+      float sum = s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, mz, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float M = fmaxf(mz, om);
+        sum = (M == -INFINITY) ? 0.f : sum * ex2f_approx((mz - M) * c) + os * ex2f_approx((om - M) * c);
+        mz = M;
+      }
+      if (lane == 0) {
+        red[warp * 2] = mz;
+        red[warp * 2 + 1] = sum;
+      }
+      fbar_sync();
+      if (tid == 0) {
+        float M = red[0];
+        for (int w = 1; w < kFW; ++w) M = fmaxf(M, red[w * 2]);
+        float S = 0.f;
+        for (int w = 0; w < kFW; ++w)
+          S += red[w * 2] == -INFINITY ? 0.f : red[w * 2 + 1] * ex2f_approx((red[w * 2] - M) * c);
+        // this CTA's partial -> the peer's slot[p]; keep a local copy in bcast[2..3]
+        st_async_peer(mapa(smem_u32(&slot[p]), peer), M, S, mapa(smem_u32(&xbar[p]), peer));
+        bcast[2] = M;
+        bcast[3] = S;
+        mbar_wait(&xbar[p], xph[p]);
+        const float2 o = slot[p];
+        // combine in f64 and run the epilogue (objective.py:243-248, 277-279); both CTAs compute the
+        // same numbers, rank 0 writes the per-token outputs
+        const double Mm = fmax((double)M, (double)o.x);
+        double Sd = 0.0;
+        if (M != -INFINITY) Sd += (double)S * exp2(((double)M - Mm) * (kLog2eF / T));
+        if (o.x != -INFINITY) Sd += (double)o.y * exp2(((double)o.x - Mm) * (kLog2eF / T));
+        const double lse = (T == 1.0 ? Mm : Mm / T) + log(Sd);
+        const int32_t tok = pf_tok;
+        double cf = 0.0;
+        if (tok < 0 || (uint64_t)tok >= a.vocab) {
+          if (rank == 0) {
+            atomicOr(a.flags, 2);
+            if (a.logp) a.logp[row] = nan("");
+            if (a.lse) a.lse[row] = lse;
+            a.term[row] = 0.0;
+            a.coef[row] = 0.0;
+          }
+        } else {
+          const double z = pf_z;
+          const double logp = __dsub_rn(T == 1.0 ? z : __ddiv_rn(z, T), lse);
+          const double lt = pf_lt, li = pf_li;
+          const double r = exp(__dsub_rn(logp, lt));
+          const double w = fmin(exp(__dsub_rn(lt, li)), a.clip.tis_cap);
+          const TripletF tv = triplet_f(r, pf_adv, a.clip);
+          cf = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(pf_norm, w), tv.slope), r), T);
+          if (rank == 0) {
+            if (!isfinite(logp)) atomicOr(a.flags, 1);
+            if (a.logp) a.logp[row] = logp;
+            if (a.lse) a.lse[row] = lse;
+            a.term[row] = __dmul_rn(w, tv.value);
+            a.coef[row] = cf;
+          }
+        }
+        bcast[0] = (float)(cf * a.grad_scale);
+        bcast[1] = (float)(-lse * kLog2eF);
+      }
+      fbar_sync();
+      xph[p] ^= 1u;
+      const float cf = bcast[0], nl = bcast[1];
+      const int64_t tok_local = (int64_t)a.tokens[row] - (int64_t)v0;
+      // pass 2: grad = cf * (onehot - 2^(z c - lse log2 e)) for this half, chunk by chunk
+      RingPos q2 = q_row;
+      for (uint32_t k = 0; k < nch; ++k) {
+        const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
+        const uint8_t* cb = buf + q2.s * kChunkBytes;
+        const uint64_t e0 = (uint64_t)k * (kChunkBytes / 2);
+        for (uint32_t v = tid; v < bytes / 16; v += kFT) {
+          const uint4 w = lds128(cb + v * 16);
+          float z[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
+                        bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
+          float g[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) g[e] = cf == 0.f ? 0.f : -cf * ex2f_approx(fmaf(z[e], c, nl));
+          const int64_t rel = tok_local - (int64_t)(e0 + (uint64_t)v * 8);
+          if (rel >= 0 && rel < 8) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (e == rel) g[e] += cf;
+          }
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 p2 = __floats2bfloat162_rn(g[2 * e], g[2 * e + 1]);
+            o[e] = *reinterpret_cast<uint32_t*>(&p2);
+          }
+          stg128_stream(grow + e0 + (uint64_t)v * 8, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[q2.s]);
+        q2.next(nslots);
+      }
+    }
+  }
+  __syncwarp();
+  cluster_sync_all();  // no CTA leaves while its peer may still st.async into it
+}
+
+}  // namespace rlk
+
+using namespace rlk;
+
+extern "C" int rlk_grpo_fused_bf16(const void* logits, uint64_t n_rows, uint64_t vocab, uint64_t row_stride,
+                                   const int64_t* row_index, const int32_t* tokens, const double* logp_train,
+                                   const double* logp_infer, const int32_t* sample_of_row, const double* adv,
+                                   const uint8_t* use, const double* temperature, const double* norm,
+                                   const rlk_clip* clip, double grad_scale, double* logp_out, double* lse_out,
+                                   double* term, double* coef, int32_t* flags, void* grad, uint64_t grad_row_stride,
+                                   void* stream) {
+  if (n_rows == 0) return RLK_OK;
+  RLK_REQUIRE(logits && tokens && logp_train && logp_infer && sample_of_row && adv && use && temperature && norm &&
+                  clip && term && coef && flags && grad,
+              "rlk_grpo_fused_bf16: NULL argument");
+  RLK_REQUIRE(vocab % 16 == 0 && vocab * 2 / 2 <= kMaxHalfBytes, "rlk_grpo_fused_bf16: vocab must be a multiple of 16 and <= %u",
+              kMaxHalfBytes);
+  RLK_REQUIRE(row_stride % 8 == 0 && grad_row_stride % 8 == 0 && ((uintptr_t)logits & 15u) == 0 &&
+                  ((uintptr_t)grad & 15u) == 0,
+              "rlk_grpo_fused_bf16: rows must be 16-byte aligned");
+  FusedArgs a;
+  a.logits = (const char*)logits;
+  a.n_rows = n_rows;
+  a.vocab = vocab;
+  a.row_stride = row_stride;
+  a.row_index = row_index;
+  a.tokens = tokens;
+  a.lp_train = logp_train;
+  a.lp_infer = logp_infer;
+  a.sample = sample_of_row;
+  a.adv = adv;
+  a.use = use;
+  a.temp = temperature;
+  a.norm = norm;
+  a.clip = *clip;
+  a.grad_scale = grad_scale;
+  a.logp = logp_out;
+  a.lse = lse_out;
+  a.term = term;
+  a.coef = coef;
+  a.flags = flags;
+  a.grad = (uint16_t*)grad;
+  a.grad_row_stride = grad_row_stride;
+  const uint32_t half_bytes = (uint32_t)(vocab);  // vocab/2 elements * 2 bytes
+  const uint32_t nch = (half_bytes + kChunkBytes - 1) / kChunkBytes;
+  a.nslots = std::max<uint32_t>(nch, std::min<uint32_t>(60u, (226u * 1024u - 1024u) / kChunkBytes));
+  const uint32_t smem = 1024 + a.nslots * kChunkBytes;
+  if (int st = cuda_status(cudaFuncSetAttribute(k_grpo_fused_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem), "cudaFuncSetAttribute"))
+    return st;
+  const uint64_t clusters = std::min<uint64_t>((n_rows + 0), (uint64_t)sm_count() / 2);
+  k_grpo_fused_bf16<<<(unsigned)(2 * std::max<uint64_t>(clusters, 1)), kFThreads, smem, (cudaStream_t)stream>>>(a);
+  return launch_status("rlk_grpo_fused_bf16");
+}

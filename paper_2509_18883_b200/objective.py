@@ -305,6 +305,40 @@ def grpo_backward(logits: torch.Tensor, batch: GRPOBatch, fwd: GRPOForward, grad
     return grad
 
 
+def grpo_forward_backward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = ClipConfig(),
+                          grad_scale: float = 1.0, *, stream=None, group=None) -> tuple[GRPOForward, torch.Tensor]:
+    """J and grad_scale * dJ/dlogits in ONE read of the logits (bf16, one row per token): the fused
+    cluster kernel `rlk_grpo_fused_bf16`.  Other dtypes / layouts fall back to K4 + K5."""
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return grpo_forward_backward(logits, batch, clip, grad_scale, group=group)
+    logits = logits.contiguous()
+    R, V = logits.shape
+    if logits.dtype != torch.bfloat16 or batch.row_index is not None or V % 16 or V > 204800:
+        fwd = grpo_forward(logits, batch, clip, group=group)
+        return fwd, grpo_backward(logits, batch, fwd, grad_scale)
+    dev = logits.device
+    f64 = dict(dtype=torch.float64, device=dev)
+    logp, lse, term, coef = (torch.empty(R, **f64) for _ in range(4))
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    grad = torch.empty_like(logits)
+    c = clip.c_struct()
+    s = L.stream_handle()
+    L.call("rlk_grpo_fused_bf16", L.ptr(logits), R, V, V, None, L.ptr(batch.tokens), L.ptr(batch.logp_train),
+           L.ptr(batch.logp_infer), L.ptr(batch.sample_of_row), L.ptr(batch.adv), L.ptr(batch.use),
+           L.ptr(batch.temperature), L.ptr(batch.norm), L.C.byref(c), float(grad_scale), L.ptr(logp), L.ptr(lse),
+           L.ptr(term), L.ptr(coef), L.ptr(flags), L.ptr(grad), V, s)
+    gs = torch.empty(batch.n_groups, **f64)
+    L.call("rlk_segment_sum_f64", L.ptr(term), L.ptr(batch.group_rows), batch.n_groups, L.ptr(gs), s)
+    if group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(gs, group=group)
+    scaled = gs / float(batch.group_size * batch.t_max)
+    tot = torch.empty(1, **f64)
+    L.call("rlk_segment_sum_f64", L.ptr(scaled), L.ptr(batch.all_groups_seg()), 1, L.ptr(tot), s)
+    return GRPOForward(tot[0] / batch.n_groups, gs, logp, lse, term, coef, flags), grad
+
+
 class GRPOTokenLoss(torch.autograd.Function):
     """Autograd wrapper: forward returns J (maximised objective); backward runs K5."""
 

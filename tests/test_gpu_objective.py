@@ -167,3 +167,23 @@ def test_bad_token_flag(cuda):
     b = O.GRPOBatch.pack([5, V + 3], [-1.0, -1.0], [-1.0, -1.0], [0, 1, 2], [1.0, -1.0], [1, 1], 2, 4, device=cuda)
     fwd = O.grpo_forward(torch.zeros((2, V), device=cuda, dtype=torch.bfloat16), b)
     assert int(fwd.flags.item()) & 2
+
+
+@pytest.mark.parametrize("V", [131072, 4096])
+def test_fused_forward_backward(cuda, V):
+    """Single-pass cluster kernel == K4 + K5 (loss, per-token outputs, bf16 gradient)."""
+    from paper_2509_18883_b200 import objective as O
+    G, S, Rps, T_max = 4, 8, 9, 16
+    logits, toks, lt, li, adv, use, cu = _synthetic_rows(Rps, S, V, G, seed=3, tau=0.8, masked=(2, 5))
+    b = O.GRPOBatch.pack(toks, lt, li, cu, adv, use, G, T_max, temperature=0.8, device=cuda)
+    lg = torch.from_numpy(logits).to(cuda, torch.bfloat16)
+    fwd, grad = O.grpo_forward_backward(lg, b, grad_scale=-1.0)
+    ref = O.grpo_forward(lg, b)
+    gref = O.grpo_backward(lg, b, ref, -1.0, grad_dtype=torch.float32)
+    assert float(fwd.objective) == pytest.approx(float(ref.objective), rel=1e-6, abs=1e-12)
+    np.testing.assert_allclose(fwd.logp.cpu().numpy(), ref.logp.cpu().numpy(), rtol=0, atol=2e-6)
+    np.testing.assert_allclose(fwd.coef.cpu().numpy(), ref.coef.cpu().numpy(), rtol=1e-5, atol=1e-12)
+    scale = float(ref.coef.abs().max())
+    np.testing.assert_allclose(grad.float().cpu().numpy(), gref.cpu().numpy(), rtol=0, atol=1e-2 * scale + 1e-12)
+    sor = np.repeat(np.arange(S), Rps)
+    assert not grad[torch.from_numpy(~use[sor].astype(bool)).to(cuda)].any()
