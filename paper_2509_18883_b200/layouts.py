@@ -52,7 +52,27 @@ def llama3_8b() -> "OrderedDict[str, tuple]":
     return out
 
 
-LAYOUTS = {"mlp10m": mlp_10m, "gpt1p3b": gpt_1p3b, "llama8b": llama3_8b}
+def longcat_560b(n_layers: int = 28) -> "OrderedDict[str, tuple]":
+    """Config 4: LongCat-Flash-560B-MoE-shaped (shapes not published, this layout is
+    an assumption): 28 layers x 512 experts x (gate, up: 2048x6144; down: 6144x2048) stored per expert
+    matrix, + attention 4 x 6144^2, router 6144x512, norms, and 131072 x 6144 embeddings / head.
+    ~5.5e11 params in ~43k tensors."""
+    d, f, e, v = 6144, 2048, 512, 131072
+    out = OrderedDict([("model.embed_tokens.weight", (v, d))])
+    for i in range(n_layers):
+        p = f"model.layers.{i}."
+        out.update([(p + "input_layernorm.weight", (d,)), (p + "post_attention_layernorm.weight", (d,))])
+        for m in ("q_proj", "k_proj", "v_proj", "o_proj"):
+            out[p + f"self_attn.{m}.weight"] = (d, d)
+        out[p + "mlp.router.weight"] = (e, d)
+        for x in range(e):
+            q = p + f"mlp.experts.{x}."
+            out.update([(q + "gate_proj.weight", (f, d)), (q + "up_proj.weight", (f, d)), (q + "down_proj.weight", (d, f))])
+    out.update([("model.norm.weight", (d,)), ("lm_head.weight", (v, d))])
+    return out
+
+
+LAYOUTS = {"mlp10m": mlp_10m, "gpt1p3b": gpt_1p3b, "llama8b": llama3_8b, "longcat560b": longcat_560b}
 
 
 def numel(shape) -> int:
