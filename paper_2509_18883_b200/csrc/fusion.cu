@@ -758,7 +758,7 @@ struct FastVec {
   }
 };
 
-template <int N, int DROP, int ERASE>
+template <int N, int DROP, int ERASE, bool UNI>
 __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_constant__ MergeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t SB = kFastSB;
@@ -867,16 +867,31 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
             // t = k * sign(vote) + 0 (exact; +0 for k = 0): t < 0 <=> entry opposes the majority.
             // Erased entries are counted from t's sign bit; survivors enter as
             // w * max(t, 0) == (w / 2) * (t + |t|) exactly (both steps are power-of-two scalings)
-            float2 acc = make_float2(0.f, 0.f);
+            if constexpr (UNI) {
+              // uniform weights w: sum_i w max(sg k_i, 0) = (w / 2) (sum_i k_i + sg sum_i |k_i|), so
+              // y = b + (w / 2) (sum k + sg sum|k|); error <= (4 + 2 (N - 1) + 1) 2^-24 (|b| + w sum|k|)
+              float2 vplain = k2[0];
 #pragma unroll
-            for (int i = 0; i < N; ++i) {
-              const float2 t2 = __ffma2_rn(k2[i], sg, make_float2(0.f, 0.f));
-              cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i], a.two);
-              cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i], a.two);
-              const float2 tp = __fadd2_rn(t2, make_float2(fabsf(t2.x), fabsf(t2.y)));
-              acc = __ffma2_rn(make_float2(wh32[i], wh32[i]), tp, acc);
+              for (int i = 1; i < N; ++i) vplain = (ERASE == 1) ? vv : __fadd2_rn(vplain, k2[i]);
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                const float2 t2 = __ffma2_rn(k2[i], sg, make_float2(0.f, 0.f));
+                cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i], a.two);
+                cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i], a.two);
+              }
+              y2 = __ffma2_rn(make_float2(wh32[0], wh32[0]), __ffma2_rn(sg, aa, vplain), b2);
+            } else {
+              float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                const float2 t2 = __ffma2_rn(k2[i], sg, make_float2(0.f, 0.f));
+                cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i], a.two);
+                cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i], a.two);
+                const float2 tp = __fadd2_rn(t2, make_float2(fabsf(t2.x), fabsf(t2.y)));
+                acc = __ffma2_rn(make_float2(wh32[i], wh32[i]), tp, acc);
+              }
+              y2 = __ffma2_rn(sg, acc, b2);
             }
-            y2 = __ffma2_rn(sg, acc, b2);
           } else {
             y2 = b2;
 #pragma unroll
@@ -1003,14 +1018,14 @@ static int launch_sumsq(SumsqArgs& a, cudaStream_t s) {
   return launch_status("rlk_fusion_sumsq");
 }
 
-template <int N, int DROP, int ERASE>
+template <int N, int DROP, int ERASE, bool UNI = false>
 static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
   uint32_t sb = (N + 1) * kFastSB + (DROP ? N * (kFastSB / 2 / 8) : 0);
   sb = (sb + 127) & ~127u;
   a.stage_bytes = sb;
   a.nstages = std::min<uint32_t>(8, (kSmemBudget - 1024) / sb);
   const uint32_t smem = 1024 + a.stage_bytes * a.nstages;
-  auto kern = k_merge_fast<N, DROP, ERASE>;
+  auto kern = k_merge_fast<N, DROP, ERASE, UNI>;
   int st = ensure_smem(kern, smem);
   if (st) return st;
   uint32_t grid = std::min<uint32_t>(a.plan.n_items, (uint32_t)sm_count());
@@ -1021,13 +1036,15 @@ static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
 template <int N>
 static int dispatch_fast(MergeArgs& a, cudaStream_t s) {
   const int ec = N >= 2 ? a.erase_mode : 0;
+  bool uni = true;
+  for (int i = 1; i < N; ++i) uni = uni && a.w[i] == a.w[0];
   if (a.dropout_mode == 2) {
-    if (ec == 1) return launch_merge_fast<N, 2, 1>(a, s);
-    if (ec == 2) return launch_merge_fast<N, 2, 2>(a, s);
+    if (ec == 1) return uni ? launch_merge_fast<N, 2, 1, true>(a, s) : launch_merge_fast<N, 2, 1>(a, s);
+    if (ec == 2) return uni ? launch_merge_fast<N, 2, 2, true>(a, s) : launch_merge_fast<N, 2, 2>(a, s);
     return launch_merge_fast<N, 2, 0>(a, s);
   }
-  if (ec == 1) return launch_merge_fast<N, 0, 1>(a, s);
-  if (ec == 2) return launch_merge_fast<N, 0, 2>(a, s);
+  if (ec == 1) return uni ? launch_merge_fast<N, 0, 1, true>(a, s) : launch_merge_fast<N, 0, 1>(a, s);
+  if (ec == 2) return uni ? launch_merge_fast<N, 0, 2, true>(a, s) : launch_merge_fast<N, 0, 2>(a, s);
   return launch_merge_fast<N, 0, 0>(a, s);
 }
 
