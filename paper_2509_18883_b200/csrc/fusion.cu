@@ -423,6 +423,9 @@ __global__ void k_finalize(const double* __restrict__ partials, const uint32_t* 
 // ------------------------------------------------------------------ K2: dropout keep bitmap
 __global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, uint64_t thresh, uint64_t n_bits,
                               uint32_t* __restrict__ bitmap, uint64_t words_per_row) {
+  // keep iff (mix64(c_j) >> 11) >= thresh  <=>  mix64(c_j) >= thresh << 11  (thresh <= 2^53)
+  const uint64_t t64 = thresh << 11;
+  const bool all = thresh == 0;  // p == 0: every draw kept (t64 == 0)
   const uint64_t words = (n_bits + 31) / 32;
   const uint64_t total = words * (uint64_t)n;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -431,9 +434,12 @@ __global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, u
     const uint64_t w = gw - (uint64_t)i * words;
     const uint64_t seed = i < 4 ? (&seeds_lo.x)[i] : (&seeds_hi.x)[i - 4];
     uint32_t bits = 0;
-    const uint64_t j0 = w * 32;
+    uint64_t c = seed + (w * 32 + 1) * kGamma;  // counter of draw j = 32 w (core.py:69-71)
 #pragma unroll 8
-    for (int b = 0; b < 32; ++b) bits |= (uint32_t)keep_draw(seed, j0 + b, thresh) << b;
+    for (int b = 0; b < 32; ++b) {
+      bits |= (uint32_t)(all || mix64(c) >= t64) << b;
+      c += kGamma;
+    }
     bitmap[(uint64_t)i * words_per_row + w] = bits;
   }
 }
