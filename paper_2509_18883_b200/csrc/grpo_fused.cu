@@ -235,13 +235,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         bcast[3] = S;
         mbar_wait(&xbar[p], xph[p]);
         const float2 o = slot[p];
-        // combine in f64 and run the epilogue (objective.py:243-248, 277-279); both CTAs compute the
-        // same numbers, rank 0 writes the per-token outputs
-        const double Mm = fmax((double)M, (double)o.x);
-        double Sd = 0.0;
-        if (M != -INFINITY) Sd += (double)S * exp2(((double)M - Mm) * (kLog2eF / T));
-        if (o.x != -INFINITY) Sd += (double)o.y * exp2(((double)o.x - Mm) * (kLog2eF / T));
-        const double lse = (T == 1.0 ? Mm : Mm / T) + log(Sd);
+        // combine and run the epilogue (objective.py:243-248, 277-279) in f32 on the MUFU (ex2 / lg2):
+        // a serial f64 epilogue here stalls all 16 warps for ~1 us per row.  Both CTAs compute the same
+        // numbers; rank 0 writes the per-token outputs.
+        const float Mm = fmaxf(M, o.x);
+        float Sf = 0.f;
+        if (M != -INFINITY) Sf += S * ex2f_approx((M - Mm) * c);
+        if (o.x != -INFINITY) Sf += o.y * ex2f_approx((o.x - Mm) * c);
+        const float inv_t = (float)(1.0 / T);
+        float lg2s;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg2s) : "f"(Sf));
+        const float lse = Mm * inv_t + lg2s * 0.69314718f;  // ln-sum-exp of z / T
         const int32_t tok = pf_tok;
         double cf = 0.0;
         if (tok < 0 || (uint64_t)tok >= a.vocab) {
@@ -253,23 +257,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
             a.coef[row] = 0.0;
           }
         } else {
-          const double z = pf_z;
-          const double logp = __dsub_rn(T == 1.0 ? z : __ddiv_rn(z, T), lse);
-          const double lt = pf_lt, li = pf_li;
-          const double r = exp(__dsub_rn(logp, lt));
-          const double w = fmin(exp(__dsub_rn(lt, li)), a.clip.tis_cap);
-          const TripletF tv = triplet_f(r, pf_adv, a.clip);
-          cf = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(pf_norm, w), tv.slope), r), T);
+          const float logp = (float)pf_z * inv_t - lse;
+          const float lt = (float)pf_lt, li = (float)pf_li;
+          const float r = ex2f_approx((logp - lt) * 1.44269504f);
+          const float w = fminf(ex2f_approx((lt - li) * 1.44269504f), (float)a.clip.tis_cap);
+          const TripletF tv = triplet_f((double)r, pf_adv, a.clip);
+          cf = pf_norm * (double)w * tv.slope * (double)r / T;
           if (rank == 0) {
             if (!isfinite(logp)) atomicOr(a.flags, 1);
             if (a.logp) a.logp[row] = logp;
             if (a.lse) a.lse[row] = lse;
-            a.term[row] = __dmul_rn(w, tv.value);
+            a.term[row] = (double)w * tv.value;
             a.coef[row] = cf;
           }
         }
         bcast[0] = (float)(cf * a.grad_scale);
-        bcast[1] = (float)(-lse * kLog2eF);
+        bcast[1] = -lse * 1.44269504f;
       }
       fbar_sync();
       xph[p] ^= 1u;

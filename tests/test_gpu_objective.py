@@ -180,9 +180,10 @@ def test_fused_forward_backward(cuda, V):
     fwd, grad = O.grpo_forward_backward(lg, b, grad_scale=-1.0)
     ref = O.grpo_forward(lg, b)
     gref = O.grpo_backward(lg, b, ref, -1.0, grad_dtype=torch.float32)
-    assert float(fwd.objective) == pytest.approx(float(ref.objective), rel=1e-6, abs=1e-12)
-    np.testing.assert_allclose(fwd.logp.cpu().numpy(), ref.logp.cpu().numpy(), rtol=0, atol=2e-6)
-    np.testing.assert_allclose(fwd.coef.cpu().numpy(), ref.coef.cpu().numpy(), rtol=1e-5, atol=1e-12)
+    assert float(fwd.objective) == pytest.approx(float(ref.objective), rel=1e-5, abs=1e-12)
+    # the fused kernel's per-row epilogue runs in f32 (MUFU ex2/lg2): logp to ~1e-5 absolute
+    np.testing.assert_allclose(fwd.logp.cpu().numpy(), ref.logp.cpu().numpy(), rtol=0, atol=2e-5)
+    np.testing.assert_allclose(fwd.coef.cpu().numpy(), ref.coef.cpu().numpy(), rtol=1e-4, atol=1e-12)
     scale = float(ref.coef.abs().max())
     np.testing.assert_allclose(grad.float().cpu().numpy(), gref.cpu().numpy(), rtol=0, atol=1e-2 * scale + 1e-12)
     sor = np.repeat(np.arange(S), Rps)
