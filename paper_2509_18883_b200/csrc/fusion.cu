@@ -427,12 +427,10 @@ __global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, u
   const uint64_t t64 = thresh << 11;
   const bool all = thresh == 0;  // p == 0: every draw kept (t64 == 0)
   const uint64_t words = (n_bits + 31) / 32;
-  const uint64_t total = words * (uint64_t)n;
+  const int i = blockIdx.y;  // expert (grid.y = N): no 64-bit division per word
+  const uint64_t seed = i < 4 ? (&seeds_lo.x)[i] : (&seeds_hi.x)[i - 4];
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t gw = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; gw < total; gw += stride) {
-    const int i = (int)(gw / words);
-    const uint64_t w = gw - (uint64_t)i * words;
-    const uint64_t seed = i < 4 ? (&seeds_lo.x)[i] : (&seeds_hi.x)[i - 4];
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += stride) {
     uint32_t bits = 0;
     uint64_t c = seed + (w * 32 + 1) * kGamma;  // counter of draw j = 32 w (core.py:69-71)
 #pragma unroll 8
@@ -1176,10 +1174,11 @@ int rlk_fusion_mask_bitmap(const uint64_t* child_seeds, int n_experts, uint64_t 
   if (n_bits == 0) return RLK_OK;
   ulonglong4 lo = make_ulonglong4(0, 0, 0, 0), hi = make_ulonglong4(0, 0, 0, 0);
   for (int i = 0; i < n_experts; ++i) (i < 4 ? (&lo.x)[i] : (&hi.x)[i - 4]) = child_seeds[i];
-  const uint64_t total = ((n_bits + 31) / 32) * (uint64_t)n_experts;
-  const uint64_t blocks = (total + 255) / 256;
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(blocks, (uint64_t)sm_count() * 16);
-  k_mask_bitmap<<<grid, 256, 0, (cudaStream_t)stream>>>(lo, hi, n_experts, thresh, n_bits, bitmap, words_per_row);
+  const uint64_t words = (n_bits + 31) / 32;
+  const uint64_t blocks = (words + 255) / 256;
+  const uint32_t gx = (uint32_t)std::min<uint64_t>(blocks, (uint64_t)sm_count() * 16 / n_experts + 1);
+  k_mask_bitmap<<<dim3(gx, n_experts), 256, 0, (cudaStream_t)stream>>>(lo, hi, n_experts, thresh, n_bits, bitmap,
+                                                                    words_per_row);
   return launch_status("rlk_fusion_mask_bitmap");
 }
 

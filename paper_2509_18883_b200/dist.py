@@ -27,14 +27,14 @@ from .fusion import FusionCall, FusionConfig, FusionLayout, FusionStats, Piece
 def allreduce_partials(partials: torch.Tensor, group) -> torch.Tensor:
     """Exact sum of disjointly-written f64 partial slots (x + 0 == x, whatever the reduction order)."""
     import torch.distributed as dist
-    if group is not None and dist.get_world_size(group) > 1:
+    if group is not None:
         dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
     return partials
 
 
 def allreduce_counts(counts: torch.Tensor, group) -> torch.Tensor:
     import torch.distributed as dist
-    if group is not None and dist.get_world_size(group) > 1:
+    if group is not None:
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     return counts
 

@@ -277,7 +277,7 @@ class FusionCall:
                 self._launch("rlk_fusion_sumsq", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
                              int(self.delta_mode), L.ptr(self.partials), L.ptr(self.counters), self.dropout_mode,
                              seeds, self.thresh, L.ptr(self.bitmap), self.words_per_row, s)
-                if world > 1:
+                if self.group is not None:
                     # disjoint slots: the sum is exact, so norms are identical at every world size
                     from .dist import allreduce_partials
                     allreduce_partials(self.partials, self.group)
