@@ -148,7 +148,7 @@ int rlk_grpo_fused_bf16(const void* logits, uint64_t n_rows, uint64_t vocab, uin
                         double* term, double* coef, int32_t* flags, void* grad, uint64_t grad_row_stride,
                         void* stream);
 
-/* out[g] = sum of x[seg_ptr[g] .. seg_ptr[g+1]) in a fixed order (one warp per segment). */
+/* out[g] = sum of x[seg_ptr[g] .. seg_ptr[g+1]) in a fixed order (one block per segment). */
 int rlk_segment_sum_f64(const double* x, const int64_t* seg_ptr, uint64_t n_segs, double* out, void* stream);
 
 /* GRPO backward (K5).  Output row o of grad (grad_row_stride elements apart) is

@@ -695,15 +695,24 @@ __global__ void k_logsoftmax_rows(const char* logits, uint64_t n_rows, uint64_t 
   }
 }
 
+// One 256-thread block per segment: thread t sums elements t, t + 256, ... of the segment, then a
+// fixed shuffle / shared-memory tree -- the result depends only on the data, never on timing.
 __global__ void k_segment_sum(const double* __restrict__ x, const int64_t* __restrict__ seg, uint64_t n_segs,
                               double* __restrict__ out) {
-  const uint64_t g = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (g >= n_segs) return;
-  double acc = 0.0;
-  for (int64_t i = seg[g] + lane; i < seg[g + 1]; i += 32) acc += x[i];
-  acc = warp_sum_f64(acc);
-  if (lane == 0) out[g] = acc;
+  __shared__ double red[8];
+  for (uint64_t g = blockIdx.x; g < n_segs; g += gridDim.x) {
+    double acc = 0.0;
+    for (int64_t i = seg[g] + threadIdx.x; i < seg[g + 1]; i += blockDim.x) acc += x[i];
+    acc = warp_sum_f64(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = red[0];
+      for (int w = 1; w < 8; ++w) t += red[w];
+      out[g] = t;
+    }
+    __syncthreads();
+  }
 }
 
 static int grid_rows(uint64_t n_rows) {
@@ -823,8 +832,8 @@ int rlk_grpo_fwd(const void* logits, int dtype, uint64_t n_rows, uint64_t vocab,
 int rlk_segment_sum_f64(const double* x, const int64_t* seg_ptr, uint64_t n_segs, double* out, void* stream) {
   if (n_segs == 0) return RLK_OK;
   RLK_REQUIRE(x && seg_ptr && out, "rlk_segment_sum_f64: NULL argument");
-  const uint64_t grid = (n_segs + 7) / 8;
-  k_segment_sum<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(x, seg_ptr, n_segs, out);
+  const unsigned grid = (unsigned)std::min<uint64_t>(n_segs, 65535u);
+  k_segment_sum<<<grid, 256, 0, (cudaStream_t)stream>>>(x, seg_ptr, n_segs, out);
   return launch_status("rlk_segment_sum_f64");
 }
 

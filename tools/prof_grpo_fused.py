@@ -14,6 +14,7 @@ g = np.random.default_rng(0)
 b = O.GRPOBatch.pack(g.integers(0, V, R), g.normal(-12, .3, R), g.normal(-12, .3, R), [0, R // 2, R], [1., -1.],
                      [1, 1], 2, R, device=dev)
 for _ in range(3):
+    O.grpo_forward(lg, b)
     O.grpo_forward_backward(lg, b)
 torch.cuda.synchronize()
 print("ok")
