@@ -18,12 +18,11 @@ namespace rlk {
 
 constexpr int kFW = 16;                   // consumer warps
 constexpr int kFT = kFW * 32;
-constexpr int kFThreads = kFT + 32;       // + producer warp
+constexpr int kFThreads = kFT + 64;       // + producer warp + epilogue warp
 constexpr uint32_t kChunkBytes = 16384;   // TMA chunk (8192 bf16)
 constexpr uint32_t kMaxHalfBytes = 200 * 1024;
 constexpr double kLog2eF = 1.4426950408889634074;
 
-__device__ __forceinline__ void fbar_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kFT) : "memory"); }
 __device__ __forceinline__ float ex2f_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -94,21 +93,67 @@ __device__ __forceinline__ TripletF triplet_f(double r, double adv, const rlk_cl
   return {floor_v, 0.0};
 }
 
+// Pass 1 over chunk k of a half row: online max / sum of 2^(z c - m c) in (mz, s0, s1); nb = -mz c.
+struct RowAcc {
+  float mz, s0, s1, nb;
+  __device__ void reset() { mz = -INFINITY; s0 = 0.f; s1 = 0.f; nb = INFINITY; }
+  __device__ __forceinline__ void chunk(const uint8_t* cb, uint32_t bytes, float c, int tid) {
+    for (uint32_t v = tid; v < bytes / 16; v += kFT) {
+      const uint4 w = lds128(cb + v * 16);
+      float z[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
+                    bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
+      const float lm = fmaxf(fmaxf(fmaxf(z[0], z[1]), fmaxf(z[2], z[3])), fmaxf(fmaxf(z[4], z[5]), fmaxf(z[6], z[7])));
+      if (lm > mz) {
+        const float f = ex2f_approx((mz - lm) * c);
+        s0 *= f;
+        s1 *= f;
+        mz = lm;
+        nb = -mz * c;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        s0 += ex2f_approx(fmaf(z[e], c, nb));
+        s1 += ex2f_approx(fmaf(z[e + 1], c, nb));
+      }
+    }
+  }
+};
+
+// (M, S) of the lanes' (m, s) pairs: max and sum of s * 2^((m - M) c); empty pairs have m = -inf.
+__device__ __forceinline__ void warp_combine(float& mz, float& sum, float c, unsigned mask = 0xffffffffu) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(mask, mz, o), os = __shfl_xor_sync(mask, sum, o);
+    const float M = fmaxf(mz, om);
+    sum = (M == -INFINITY) ? 0.f : sum * ex2f_approx((mz - M) * c) + os * ex2f_approx((om - M) * c);
+    mz = M;
+  }
+}
+
+// Warp roles: 16 consumer warps (both passes), one producer warp (lane 0 issues TMA), one epilogue
+// warp.  Rows are software-pipelined: after pass 1 of row r the consumers hand their partials to the
+// epilogue warp (mbarrier), run pass 1 over the chunks of the next row that are already in the ring,
+// and only then wait for row r's coefficient and run its pass 2 -- the cross-CTA exchange and the
+// serial epilogue are off the consumers' critical path.
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo_fused_bf16(FusedArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  // layout: [full[nch] | empty[nch] | xbar[2] | pad] [slot[2] float2] [coef broadcast] ... 1 KiB header
+  // 1 KiB header: [full[nslots] | empty[nslots] | xbar[2] | pready[2] | cready[2]] (<= 512 B),
+  // slot[2] float2 @512, bcast[2][4] float @576, red[2][kFW][2] float @640
   const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
   const uint64_t half = a.vocab / 2;  // elements owned by this CTA (vocab % 16 == 0)
   const uint64_t v0 = rank * half;
   const uint32_t half_bytes = (uint32_t)(half * 2);
   const uint32_t nch = (half_bytes + kChunkBytes - 1) / kChunkBytes;  // chunks per half row
   const uint32_t nslots = a.nslots;  // ring slots >= nch: the producer runs ahead into the next row
+  const uint32_t pre = min(nch, nslots - nch);  // next-row chunks that fit beside the current row
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + nslots;
   uint64_t* xbar = empty + nslots;
+  uint64_t* pready = xbar + 2;
+  uint64_t* cready = pready + 2;
   float2* slot = reinterpret_cast<float2*>(smem + 512);
   float* bcast = reinterpret_cast<float*>(smem + 576);
-  float* red = reinterpret_cast<float*>(smem + 640);  // [kFW][2]
+  float* red = reinterpret_cast<float*>(smem + 640);
   uint8_t* buf = smem + 1024;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   if (threadIdx.x == 0) {
@@ -116,28 +161,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       mbar_init(&full[k], 1);
       mbar_init(&empty[k], kFW);
     }
-    mbar_init(&xbar[0], 1);
-    mbar_init(&xbar[1], 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&xbar[k], 1);
+      mbar_init(&pready[k], kFW);
+      mbar_init(&cready[k], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
   cluster_sync_all();  // peers' barriers exist before any st.async targets them
 
   auto active = [&](uint64_t row) { return a.use[a.sample[row]] != 0; };
-  auto row_ptr = [&](uint64_t row) {
-    const uint64_t rr = a.row_index ? (uint64_t)a.row_index[row] : row;
-    return a.logits + (rr * a.row_stride + v0) * 2;
-  };
+  auto lrow = [&](uint64_t row) { return a.row_index ? (uint64_t)a.row_index[row] : row; };
   const uint64_t row0 = cluster_id_x(), rstep = n_clusters_x();
 
   if (warp == kFW) {
-    // ---------------- producer: chunk k of every active row into buffer slot k
+    // ---------------- producer: chunk k of every active row into the next ring slot
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       RingPos q;
       for (uint64_t row = row0; row < a.n_rows; row += rstep) {
         if (!active(row)) continue;
-        const char* src = row_ptr(row);
+        const char* src = a.logits + (lrow(row) * a.row_stride + v0) * 2;
         for (uint32_t k = 0; k < nch; ++k) {
           const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
           mbar_wait(&empty[q.s], q.ph ^ 1u);
@@ -147,97 +192,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         }
       }
     }
-  } else {
-    // ---------------- consumers
-    RingPos q;
-    uint32_t xph[2] = {0u, 0u};
-    uint64_t it = 0;  // active rows seen: slot / exchange-barrier parity alternates strictly
+  } else if (warp == kFW + 1) {
+    // ---------------- epilogue warp: combine partials, exchange with the peer, per-row outputs
+    uint32_t ph[2] = {0u, 0u};
+    uint64_t it = 0;
     for (uint64_t row = row0; row < a.n_rows; row += rstep) {
-      uint16_t* grow = a.grad + (a.row_index ? (uint64_t)a.row_index[row] : row) * a.grad_row_stride + v0;
-      if (!active(row)) {  // objective.py:240-241 / 275-276: no contribution, zero gradient
-        for (uint64_t b = (uint64_t)tid * 8; b < half; b += (uint64_t)kFT * 8)
-          stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
-        if (rank == 0 && tid == 0) {
-          if (a.logp) a.logp[row] = 0.0;
-          if (a.lse) a.lse[row] = 0.0;
-          a.term[row] = 0.0;
-          a.coef[row] = 0.0;
-        }
-        continue;
-      }
+      if (!active(row)) continue;
       const uint32_t p = (uint32_t)(it++ & 1u);
       const int32_t s_id = a.sample[row];
       const double T = a.temp[s_id];
       const float c = (float)(kLog2eF / T);
-      // epilogue operands are fetched now, so their latency hides behind pass 1
-      int32_t pf_tok = 0;
-      double pf_z = 0.0, pf_lt = 0.0, pf_li = 0.0, pf_adv = 0.0, pf_norm = 0.0;
-      if (tid == 0) {
-        mbar_arrive_expect_tx(&xbar[p], 8);  // the peer's partial lands in slot[p]
-        pf_tok = a.tokens[row];
-        pf_lt = a.lp_train[row];
-        pf_li = a.lp_infer[row];
-        pf_adv = a.adv[s_id];
-        pf_norm = a.norm[s_id];
-        if (pf_tok >= 0 && (uint64_t)pf_tok < a.vocab)
-          pf_z = load_f64<RLK_BF16>(a.logits + (a.row_index ? (uint64_t)a.row_index[row] : row) * a.row_stride * 2,
-                                    (uint64_t)pf_tok);
-      }
-      // pass 1: online max / sum over this half
-      float mz = -INFINITY, s0 = 0.f, s1 = 0.f, nb = INFINITY;
-      const RingPos q_row = q;
-      for (uint32_t k = 0; k < nch; ++k) {
-        mbar_wait(&full[q.s], q.ph);
-        const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
-        const uint8_t* cb = buf + q.s * kChunkBytes;
-        q.next(nslots);
-        for (uint32_t v = tid; v < bytes / 16; v += kFT) {
-          const uint4 w = lds128(cb + v * 16);
-          float z[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
-                        bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
-          const float lm = fmaxf(fmaxf(fmaxf(z[0], z[1]), fmaxf(z[2], z[3])), fmaxf(fmaxf(z[4], z[5]), fmaxf(z[6], z[7])));
-          if (lm > mz) {
-            const float f = ex2f_approx((mz - lm) * c);
-            s0 *= f;
-            s1 *= f;
-            mz = lm;
-            nb = -mz * c;
-          }
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            s0 += ex2f_approx(fmaf(z[e], c, nb));
-            s1 += ex2f_approx(fmaf(z[e + 1], c, nb));
-          }
-        }
-      }
-      float sum = s0 + s1;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float om = __shfl_xor_sync(0xffffffffu, mz, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
-        const float M = fmaxf(mz, om);
-        sum = (M == -INFINITY) ? 0.f : sum * ex2f_approx((mz - M) * c) + os * ex2f_approx((om - M) * c);
-        mz = M;
-      }
+      int32_t tok = 0;
+      double zt = 0.0, lt64 = 0.0, li64 = 0.0, adv = 0.0, nrm = 0.0;
       if (lane == 0) {
-        red[warp * 2] = mz;
-        red[warp * 2 + 1] = sum;
+        mbar_arrive_expect_tx(&xbar[p], 8);  // the peer's partial lands in slot[p]
+        tok = a.tokens[row];
+        lt64 = a.lp_train[row];
+        li64 = a.lp_infer[row];
+        adv = a.adv[s_id];
+        nrm = a.norm[s_id];
+        if (tok >= 0 && (uint64_t)tok < a.vocab) zt = load_f64<RLK_BF16>(a.logits + lrow(row) * a.row_stride * 2, (uint64_t)tok);
       }
-      fbar_sync();
-      if (tid == 0) {
-        float M = red[0];
-        for (int w = 1; w < kFW; ++w) M = fmaxf(M, red[w * 2]);
-        float S = 0.f;
-        for (int w = 0; w < kFW; ++w)
-          S += red[w * 2] == -INFINITY ? 0.f : red[w * 2 + 1] * ex2f_approx((red[w * 2] - M) * c);
-        // this CTA's partial -> the peer's slot[p]; keep a local copy in bcast[2..3]
+      mbar_wait(&pready[p], ph[p]);
+      float M = -INFINITY, S = 0.f;
+      if (lane < kFW) {
+        M = red[(p * kFW + lane) * 2];
+        S = red[(p * kFW + lane) * 2 + 1];
+      }
+      warp_combine(M, S, c);
+      if (lane == 0) {
         st_async_peer(mapa(smem_u32(&slot[p]), peer), M, S, mapa(smem_u32(&xbar[p]), peer));
-        bcast[2] = M;
-        bcast[3] = S;
-        mbar_wait(&xbar[p], xph[p]);
+        mbar_wait(&xbar[p], ph[p]);
         const float2 o = slot[p];
-        // combine and run the epilogue (objective.py:243-248, 277-279) in f32 on the MUFU (ex2 / lg2):
-        // a serial f64 epilogue here stalls all 16 warps for ~1 us per row.  Both CTAs compute the same
-        // numbers; rank 0 writes the per-token outputs.
+        // combine and run the epilogue (objective.py:243-248, 277-279) in f32 on the MUFU (ex2 / lg2).
+        // Both CTAs compute the same numbers; rank 0 writes the per-token outputs.
         const float Mm = fmaxf(M, o.x);
         float Sf = 0.f;
         if (M != -INFINITY) Sf += S * ex2f_approx((M - Mm) * c);
@@ -246,7 +234,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         float lg2s;
         asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg2s) : "f"(Sf));
         const float lse = Mm * inv_t + lg2s * 0.69314718f;  // ln-sum-exp of z / T
-        const int32_t tok = pf_tok;
         double cf = 0.0;
         if (tok < 0 || (uint64_t)tok >= a.vocab) {
           if (rank == 0) {
@@ -257,12 +244,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
             a.coef[row] = 0.0;
           }
         } else {
-          const float logp = (float)pf_z * inv_t - lse;
-          const float lt = (float)pf_lt, li = (float)pf_li;
+          const float logp = (float)zt * inv_t - lse;
+          const float lt = (float)lt64, li = (float)li64;
           const float r = ex2f_approx((logp - lt) * 1.44269504f);
           const float w = fminf(ex2f_approx((lt - li) * 1.44269504f), (float)a.clip.tis_cap);
-          const TripletF tv = triplet_f((double)r, pf_adv, a.clip);
-          cf = pf_norm * (double)w * tv.slope * (double)r / T;
+          const TripletF tv = triplet_f((double)r, adv, a.clip);
+          cf = nrm * (double)w * tv.slope * (double)r / T;
           if (rank == 0) {
             if (!isfinite(logp)) atomicOr(a.flags, 1);
             if (a.logp) a.logp[row] = logp;
@@ -271,14 +258,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
             a.coef[row] = cf;
           }
         }
-        bcast[0] = (float)(cf * a.grad_scale);
-        bcast[1] = -lse * 1.44269504f;
+        bcast[p * 4 + 0] = (float)(cf * a.grad_scale);
+        bcast[p * 4 + 1] = -lse * 1.44269504f;
+        mbar_arrive(&cready[p]);
       }
-      fbar_sync();
-      xph[p] ^= 1u;
-      const float cf = bcast[0], nl = bcast[1];
+      ph[p] ^= 1u;
+      __syncwarp();
+    }
+  } else {
+    // ---------------- consumers
+    uint32_t cph[2] = {0u, 0u};
+    uint64_t it = 0;
+    RingPos q;        // next ring position to wait on (pass 1)
+    RowAcc acc;
+    acc.reset();
+    uint32_t done = 0;  // chunks of the current row already reduced by the previous iteration's pre-pass
+    auto next_active = [&](uint64_t row) {
+      // zero the gradient of inactive rows on the way (objective.py:240-241 / 275-276)
+      for (; row < a.n_rows; row += rstep) {
+        if (active(row)) return row;
+        uint16_t* grow = a.grad + lrow(row) * a.grad_row_stride + v0;
+        for (uint64_t b = (uint64_t)tid * 8; b < half; b += (uint64_t)kFT * 8) stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
+        if (rank == 0 && tid == 0) {
+          if (a.logp) a.logp[row] = 0.0;
+          if (a.lse) a.lse[row] = 0.0;
+          a.term[row] = 0.0;
+          a.coef[row] = 0.0;
+        }
+      }
+      return row;
+    };
+    uint64_t row = next_active(row0);
+    RingPos q_row = q;  // ring position of the current row's chunk 0
+    while (row < a.n_rows) {
+      const uint32_t p = (uint32_t)(it++ & 1u);
+      const float c = (float)(kLog2eF / a.temp[a.sample[row]]);
+      // pass 1 (rest of the row)
+      for (uint32_t k = done; k < nch; ++k) {
+        mbar_wait(&full[q.s], q.ph);
+        acc.chunk(buf + q.s * kChunkBytes, min(kChunkBytes, half_bytes - k * kChunkBytes), c, tid);
+        q.next(nslots);
+      }
+      float mz = acc.mz, sum = acc.s0 + acc.s1;
+      warp_combine(mz, sum, c);
+      if (lane == 0) {
+        red[(p * kFW + warp) * 2] = mz;
+        red[(p * kFW + warp) * 2 + 1] = sum;
+        mbar_arrive(&pready[p]);
+      }
+      // pass 1 of the next active row over the chunks already in the ring
+      const uint64_t nrow = next_active(row + rstep);
+      const RingPos q_next = q;
+      acc.reset();
+      done = 0;
+      if (nrow < a.n_rows) {
+        const float cn = (float)(kLog2eF / a.temp[a.sample[nrow]]);
+        for (; done < pre; ++done) {
+          mbar_wait(&full[q.s], q.ph);
+          acc.chunk(buf + q.s * kChunkBytes, min(kChunkBytes, half_bytes - done * kChunkBytes), cn, tid);
+          q.next(nslots);
+        }
+      }
+      // pass 2 of this row: grad = cf * (onehot - 2^(z c - lse log2 e)), chunk by chunk
+      mbar_wait(&cready[p], cph[p]);
+      cph[p] ^= 1u;
+      const float cf = bcast[p * 4 + 0], nl = bcast[p * 4 + 1];
+      uint16_t* grow = a.grad + lrow(row) * a.grad_row_stride + v0;
       const int64_t tok_local = (int64_t)a.tokens[row] - (int64_t)v0;
-      // pass 2: grad = cf * (onehot - 2^(z c - lse log2 e)) for this half, chunk by chunk
       RingPos q2 = q_row;
       for (uint32_t k = 0; k < nch; ++k) {
         const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
@@ -309,6 +355,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         if (lane == 0) mbar_arrive(&empty[q2.s]);
         q2.next(nslots);
       }
+      row = nrow;
+      q_row = q_next;
     }
   }
   __syncwarp();
