@@ -93,31 +93,64 @@ __device__ __forceinline__ TripletF triplet_f(double r, double adv, const rlk_cl
   return {floor_v, 0.0};
 }
 
-// Pass 1 over chunk k of a half row: online max / sum of 2^(z c - m c) in (mz, s0, s1); nb = -mz c.
+__device__ __forceinline__ void unpack8(const uint4 w, float* z) {
+  z[0] = bf16_lo(w.x); z[1] = bf16_hi(w.x); z[2] = bf16_lo(w.y); z[3] = bf16_hi(w.y);
+  z[4] = bf16_lo(w.z); z[5] = bf16_hi(w.z); z[6] = bf16_lo(w.w); z[7] = bf16_hi(w.w);
+}
+
+// Pass 1 over one chunk of a half row: online max / sum of 2^(z c - m c) in (mz, s[4]); nb = -mz c.
+// Two 16-byte vectors per thread per step (a full chunk is exactly two): one max test per 16 logits.
 struct RowAcc {
-  float mz, s0, s1, nb;
-  __device__ void reset() { mz = -INFINITY; s0 = 0.f; s1 = 0.f; nb = INFINITY; }
-  __device__ __forceinline__ void chunk(const uint8_t* cb, uint32_t bytes, float c, int tid) {
-    for (uint32_t v = tid; v < bytes / 16; v += kFT) {
-      const uint4 w = lds128(cb + v * 16);
-      float z[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
-                    bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
-      const float lm = fmaxf(fmaxf(fmaxf(z[0], z[1]), fmaxf(z[2], z[3])), fmaxf(fmaxf(z[4], z[5]), fmaxf(z[6], z[7])));
-      if (lm > mz) {
-        const float f = ex2f_approx((mz - lm) * c);
-        s0 *= f;
-        s1 *= f;
-        mz = lm;
-        nb = -mz * c;
-      }
-#pragma unroll
-      for (int e = 0; e < 8; e += 2) {
-        s0 += ex2f_approx(fmaf(z[e], c, nb));
-        s1 += ex2f_approx(fmaf(z[e + 1], c, nb));
-      }
-    }
+  float mz, s[4], nb;
+  __device__ void reset() {
+    mz = -INFINITY;
+    s[0] = s[1] = s[2] = s[3] = 0.f;
+    nb = INFINITY;
   }
+  template <int NV>
+  __device__ __forceinline__ void step(const uint8_t* cb, uint32_t v, float c) {
+    float z[8 * NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) unpack8(lds128(cb + (v + u * kFT) * 16), z + 8 * u);
+    float lm = z[0];
+#pragma unroll
+    for (int e = 1; e < 8 * NV; ++e) lm = fmaxf(lm, z[e]);
+    if (lm > mz) {
+      const float f = ex2f_approx((mz - lm) * c);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s[j] *= f;
+      mz = lm;
+      nb = -mz * c;
+    }
+#pragma unroll
+    for (int e = 0; e < 8 * NV; ++e) s[e & 3] += ex2f_approx(fmaf(z[e], c, nb));
+  }
+  __device__ __forceinline__ void chunk(const uint8_t* cb, uint32_t bytes, float c, int tid) {
+    const uint32_t nv = bytes / 16;
+    uint32_t v = tid;
+    for (; v + kFT < nv; v += 2 * kFT) step<2>(cb, v, c);
+    if (v < nv) step<1>(cb, v, c);
+  }
+  __device__ __forceinline__ float sum() const { return (s[0] + s[1]) + (s[2] + s[3]); }
 };
+
+// Pass 2 over one chunk: grad = -cf * 2^(z c + nl) (the one-hot term is patched by the owner thread).
+template <int NV>
+__device__ __forceinline__ void grad_step(const uint8_t* cb, uint32_t v, float c, float ncf, float nl, uint16_t* gout) {
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    float z[8];
+    unpack8(lds128(cb + (v + u * kFT) * 16), z);
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(ncf * ex2f_approx(fmaf(z[2 * e], c, nl)),
+                                                ncf * ex2f_approx(fmaf(z[2 * e + 1], c, nl)));
+      o[e] = *reinterpret_cast<uint32_t*>(&p2);
+    }
+    stg128_stream(gout + (uint64_t)(v + u * kFT) * 8, make_uint4(o[0], o[1], o[2], o[3]));
+  }
+}
 
 // (M, S) of the lanes' (m, s) pairs: max and sum of s * 2^((m - M) c); empty pairs have m = -inf.
 __device__ __forceinline__ void warp_combine(float& mz, float& sum, float c, unsigned mask = 0xffffffffu) {
@@ -299,7 +332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         acc.chunk(buf + q.s * kChunkBytes, min(kChunkBytes, half_bytes - k * kChunkBytes), c, tid);
         q.next(nslots);
       }
-      float mz = acc.mz, sum = acc.s0 + acc.s1;
+      float mz = acc.mz, sum = acc.sum();
       warp_combine(mz, sum, c);
       if (lane == 0) {
         red[(p * kFW + warp) * 2] = mz;
@@ -324,32 +357,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       cph[p] ^= 1u;
       const float cf = bcast[p * 4 + 0], nl = bcast[p * 4 + 1];
       uint16_t* grow = a.grad + lrow(row) * a.grad_row_stride + v0;
+      // the chunk / vector / thread that holds the target token's logit (the one-hot term)
       const int64_t tok_local = (int64_t)a.tokens[row] - (int64_t)v0;
+      const bool tok_here = tok_local >= 0 && tok_local < (int64_t)half;
+      const uint32_t tok_chunk = tok_here ? (uint32_t)(tok_local / (kChunkBytes / 2)) : 0xffffffffu;
+      const uint32_t tok_vec = tok_here ? (uint32_t)(tok_local % (kChunkBytes / 2)) / 8 : 0u;
       RingPos q2 = q_row;
       for (uint32_t k = 0; k < nch; ++k) {
         const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
         const uint8_t* cb = buf + q2.s * kChunkBytes;
-        const uint64_t e0 = (uint64_t)k * (kChunkBytes / 2);
-        for (uint32_t v = tid; v < bytes / 16; v += kFT) {
-          const uint4 w = lds128(cb + v * 16);
-          float z[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
-                        bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
-          float g[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) g[e] = cf == 0.f ? 0.f : -cf * ex2f_approx(fmaf(z[e], c, nl));
-          const int64_t rel = tok_local - (int64_t)(e0 + (uint64_t)v * 8);
-          if (rel >= 0 && rel < 8) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (e == rel) g[e] += cf;
+        uint16_t* gout = grow + (uint64_t)k * (kChunkBytes / 2);
+        const uint32_t nv = bytes / 16;
+        if (cf == 0.f) {  // no gradient for this row (objective.py:277-279 with coef 0)
+          for (uint32_t v = tid; v < nv; v += kFT) stg128_stream(gout + (uint64_t)v * 8, make_uint4(0, 0, 0, 0));
+        } else {
+          uint32_t v = tid;
+          for (; v + kFT < nv; v += 2 * kFT) grad_step<2>(cb, v, c, -cf, nl, gout);
+          if (v < nv) grad_step<1>(cb, v, c, -cf, nl, gout);
+          if (k == tok_chunk && tok_vec % kFT == (uint32_t)tid) {
+            // same thread, after its vector store: cf * (1 - softmax) at the target
+            const uint32_t e = (uint32_t)(tok_local % (kChunkBytes / 2));
+            const float z = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(cb)[e] << 16);
+            const float g = cf - cf * ex2f_approx(fmaf(z, c, nl));
+            __nv_bfloat16 hb = __float2bfloat16_rn(g);
+            gout[e] = *reinterpret_cast<uint16_t*>(&hb);
           }
-          uint32_t o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 p2 = __floats2bfloat162_rn(g[2 * e], g[2 * e + 1]);
-            o[e] = *reinterpret_cast<uint32_t*>(&p2);
-          }
-          stg128_stream(grow + e0 + (uint64_t)v * 8, make_uint4(o[0], o[1], o[2], o[3]));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[q2.s]);
