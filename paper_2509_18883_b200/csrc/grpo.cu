@@ -11,6 +11,8 @@
 // A logits row (V = 131072 bf16 = 256 KiB) is streamed through a TMA bulk-copy ring by one producer
 // lane; eight consumer warps keep a per-thread (max, sum 2^(z*c - max*c)) pair in f32 (c = log2(e) / T,
 // MUFU.EX2 per logit), combined with shuffles at the end of the row.  The epilogue runs in f64.
+#include <type_traits>
+
 #include "common.cuh"
 #include "capi_internal.h"
 #include "pipeline.cuh"
@@ -347,12 +349,14 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd_stream(FwdArgs a, flo
     if (!active(row)) continue;
     const char* rowp = addr(row);
     const float c = (float)(kLog2e / a.temp[a.sample[row]]);
-    float mz = -INFINITY, sum = 0.f, sum2 = 0.f, nb = INFINITY;
+    float mz = -INFINITY, sum = 0.f, sum2 = 0.f, sum3 = 0.f, sum4 = 0.f, nb = INFINITY;
     auto take = [&](float z) {
       if (z > mz) {
         const float f = ex2_approx((mz - z) * c);
         sum *= f;
         sum2 *= f;
+        sum3 *= f;
+        sum4 *= f;
         mz = z;
         nb = -mz * c;
       }
@@ -368,25 +372,35 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd_stream(FwdArgs a, flo
         mbar_wait(&r.full[s], ph);
         const uint8_t* sb = r.buf + s * r.stage_bytes;
         const uint32_t nvec = main_bytes / 16;
-        for (uint32_t v = tid; v < nvec; v += kGT) {
-          float z[VEC];
-          RowVec<DT>::f32(lds128(sb + v * 16), z);
-          float lm = fmaxf(z[0], z[1]);
+        // two 16-byte vectors per step: one max test per 2 VEC logits, four independent sums
+        auto step = [&](uint32_t v, auto nv_tag) {
+          constexpr int NV = decltype(nv_tag)::value;
+          float z[VEC * NV];
 #pragma unroll
-          for (int e = 2; e < VEC; e += 2) lm = fmaxf(lm, fmaxf(z[e], z[e + 1]));
+          for (int u = 0; u < NV; ++u) RowVec<DT>::f32(lds128(sb + (v + u * kGT) * 16), z + VEC * u);
+          float lm = z[0];
+#pragma unroll
+          for (int e = 1; e < VEC * NV; ++e) lm = fmaxf(lm, z[e]);
           if (lm > mz) {
             const float f = ex2_approx((mz - lm) * c);
             sum *= f;
             sum2 *= f;
+            sum3 *= f;
+            sum4 *= f;
             mz = lm;
             nb = -mz * c;
           }
 #pragma unroll
-          for (int e = 0; e < VEC; e += 2) {
+          for (int e = 0; e < VEC * NV; e += 4) {
             sum += ex2_approx(fmaf(z[e], c, nb));
             sum2 += ex2_approx(fmaf(z[e + 1], c, nb));
+            sum3 += ex2_approx(fmaf(z[e + 2], c, nb));
+            sum4 += ex2_approx(fmaf(z[e + 3], c, nb));
           }
-        }
+        };
+        uint32_t v = tid;
+        for (; v + kGT < nvec; v += 2 * kGT) step(v, std::integral_constant<int, 2>());
+        if (v < nvec) step(v, std::integral_constant<int, 1>());
         for (uint32_t e = main_bytes / ESZ + tid; e < bytes / ESZ; e += kGT)
           take((float)load_f64<DT>(rowp, off / ESZ + e));
         __syncwarp();
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd_stream(FwdArgs a, flo
         q.next(r.nstages);
       }
     }
-    sum += sum2;
+    sum = (sum + sum2) + (sum3 + sum4);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float om = __shfl_xor_sync(0xffffffffu, mz, o), os = __shfl_xor_sync(0xffffffffu, sum, o);
