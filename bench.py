@@ -377,6 +377,47 @@ def grpo_bench(args, rank, world, local, group):
     kern = {k: statistics.mean(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
     kmax = dict(zip(kern, max_over_ranks(list(kern.values()), group)))
     out.update(kern=kmax, rows_per_launch=rows, tokens=G * T, V=V)
+
+    # SURVEY 8(d) variants (not in the headline): temperature 0.7; 2 of 16 samples masked (12.5 %);
+    # ragged lengths ~ U[T/2, T] (seeded).  Tokens counted = unmasked tokens actually read.
+    if not args.quick:
+        lens_rng = np.random.default_rng(100 + rank)
+
+        def variant(tau=1.0, masked=(), ragged=False):
+            plans, counted = [], 0
+            for k in range(n_chunks):
+                samples = mine[k * chunk:(k + 1) * chunk]
+                lens = (lens_rng.integers(T // 2, T + 1, len(samples)) if ragged else np.full(len(samples), T))
+                use = np.array([0 if sidx in masked else 1 for sidx in samples], np.uint8)
+                counted += int(sum(n for n, u in zip(lens, use) if u))
+                n_rows = int(lens.sum())
+                bt = O.GRPOBatch.pack(toks[:n_rows], lt[:n_rows], li[:n_rows], np.concatenate([[0], np.cumsum(lens)]),
+                                      adv[:len(samples)], use, len(samples), T, temperature=tau, device=dev)
+                plans.append((logits[:n_rows], bt))
+            res = {}
+            for bwd in (False, True):
+                def once():
+                    for lg, bt in plans:
+                        (O.grpo_forward_backward if bwd else O.grpo_forward)(lg, bt, stream=stream)
+                for _ in range(args.warmup):
+                    once()
+                barrier(group)
+                torch.cuda.synchronize(dev)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(args.steps):
+                    once()
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                ms, = max_over_ranks([e0.elapsed_time(e1) / args.steps], group)
+                res["fwd_bwd_ms" if bwd else "fwd_ms"] = ms
+            tot, = sum_over_ranks([counted], group)
+            res.update(tokens_counted=tot, tokens_per_s=tot / (res["fwd_ms"] / 1e3),
+                       fwd_bwd_tokens_per_s=tot / (res["fwd_bwd_ms"] / 1e3))
+            return res
+
+        out["variants"] = {"tau_0.7": variant(tau=0.7), "masked_12.5pct": variant(masked=(3, 11)),
+                           "ragged_lengths": variant(ragged=True)}
     del logits
     torch.cuda.empty_cache()
     return out
@@ -534,6 +575,8 @@ def main():
                         "roofline": {"bound": "hbm", "kernel": "rlk_grpo_fwd", "achieved": ach, "peak": peak,
                                      "unit": "GB/s", "frac": ach / peak, "bytes_per_token": gr["V"] * 2 + 12},
                         "kernels_ms": gr["kern"]}
+        if "variants" in gr:
+            line["grpo"]["variants"] = gr["variants"]
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line))
