@@ -242,7 +242,16 @@ def fusion_e2e(args, pieces, call, weights, stream, dev, group):
     stream.synchronize()
     world = 1 if group is None else torch.distributed.get_world_size(group)
     pipelined = world == 1
-    if pipelined:
+    api = pipelined and os.environ.get("RLK_E2E_MANUAL", "0") != "1"
+    if api:
+        # the public streaming API (loader.fuse_streaming): pinned host dicts in, pinned host dict out
+        from paper_2509_18883_b200.loader import ArraySink, ArraySource, fuse_streaming
+        names = [str(k) for k in range(len(views))]
+        api_b = {n: v[1][0] for n, v in zip(names, views)}
+        api_e = [{n: v[1][i + 1] for n, v in zip(names, views)} for i in range(N_EXPERTS)]
+        api_o = {n: v[2] for n, v in zip(names, views)}
+        numels = [v[0].numel for v in views]
+    elif pipelined:
         # consecutive tensor groups of ~2 GB of inputs; one FusionCall (plan) per group
         groups, cur, cur_b = [], [], 0
         for v in views:
@@ -260,6 +269,11 @@ def fusion_e2e(args, pieces, call, weights, stream, dev, group):
             calls.append(F.FusionCall(gp, F.FusionLayout([v[0].numel for v in gv]), N_EXPERTS, call.cfg, stream=stream))
 
     def step():
+        if api:
+            with torch.cuda.stream(stream):
+                fuse_streaming(names, numels, N_EXPERTS, ArraySource(api_b, api_e), ArraySink(api_o), call.cfg,
+                               dtype=dt, device_budget_bytes=16 << 30, group_bytes=2 << 30)
+            return
         if not pipelined:
             with torch.cuda.stream(stream):
                 for p, hv, _ in views:
@@ -309,7 +323,9 @@ def fusion_e2e(args, pieces, call, weights, stream, dev, group):
     h2d, d2h = sum_over_ranks([float(total * 2 * (N_EXPERTS + 1)), float(total * 2)], group)
     del host_in, host_out, views
     return dict(e2e_ms=ms, e2e_steps=steps, e2e_warmup=warm, h2d=int(h2d), d2h=int(d2h),
-                e2e_path=("pipelined tensor groups (H2D | fuse | D2H on 3 streams)" if pipelined
+                e2e_path=("loader.fuse_streaming (public API): pinned host dicts, 2 GiB tensor groups, "
+                          "H2D | fuse | D2H on 3 streams, FusionStats returned" if api else
+                          "pipelined tensor groups (H2D | fuse | D2H on 3 streams)" if pipelined
                           else "sharded: H2D, fuse with NCCL norm all_reduce, D2H"))
 
 

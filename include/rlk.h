@@ -188,7 +188,10 @@ int rlk_checksum64(const void* data, uint64_t n_words, uint64_t word_offset, uns
 /* ---- K7 host streaming loader (checkpoints larger than HBM) -------------------------------------
  * A ring of n_slots pinned host slots of slot_bytes each and n_threads host workers (0 = all cores).
  * h2d / d2h pipeline pageable<->pinned memcpy against cudaMemcpyAsync on `stream`; the device side of
- * a copy is complete when `stream` reaches the point of the call.  Loader state is not thread-safe:
+ * a copy is complete when `stream` reaches the point of the call.  Host ranges that are already
+ * page-locked (cudaHostAlloc / cudaHostRegister, e.g. torch pin_memory) skip the slots: one
+ * cudaMemcpyAsync on `stream`, asynchronous to the host, so such a buffer must stay valid (and, for
+ * d2h, unread) until `stream` reaches the call.  Loader state is not thread-safe:
  * one loader per host thread.  Replaces: no reference counterpart (the reference holds everything in
  * RAM as float64); the on-disk format it feeds is SPEC.md:588/727 (see loader.py). */
 void* rlk_loader_create(uint64_t slot_bytes, int n_slots, int n_threads);

@@ -19,6 +19,7 @@
 #include <cstring>
 #include <algorithm>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -118,17 +119,53 @@ class Pool {
   bool stop_ = false;
 };
 
+// Slots and workers are created on first use: a loader that only ever sees page-locked buffers (direct
+// DMA) costs no pinned allocation and no threads.
 struct Loader {
   uint64_t slot_bytes;
+  int n_slots, n_threads;
   std::vector<void*> slots;
   std::vector<cudaEvent_t> events;
   std::vector<bool> armed;
-  Pool pool;
+  std::unique_ptr<Pool> pool;
   int next = 0;
-  Loader(uint64_t sb, int n, int threads) : slot_bytes(sb), pool(threads) {}
+  Loader(uint64_t sb, int n, int threads) : slot_bytes(sb), n_slots(n), n_threads(threads) {}
 };
 
+int ensure_slots(Loader* L) {
+  if (!L->slots.empty()) return RLK_OK;
+  for (int i = 0; i < L->n_slots; ++i) {
+    void* p = nullptr;
+    cudaEvent_t ev;
+    cudaError_t e = cudaHostAlloc(&p, L->slot_bytes, cudaHostAllocDefault);
+    if (e == cudaSuccess) {
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) cudaFreeHost(p);
+    }
+    if (e != cudaSuccess) {
+      for (size_t k = 0; k < L->slots.size(); ++k) {
+        cudaFreeHost(L->slots[k]);
+        cudaEventDestroy(L->events[k]);
+      }
+      L->slots.clear();
+      L->events.clear();
+      L->armed.clear();
+      return fail("rlk_loader: pinned slot allocation", e);
+    }
+    L->slots.push_back(p);
+    L->events.push_back(ev);
+    L->armed.push_back(false);
+  }
+  return RLK_OK;
+}
+
+Pool& pool(Loader* L) {
+  if (!L->pool) L->pool.reset(new Pool(L->n_threads));
+  return *L->pool;
+}
+
 int acquire(Loader* L, int& slot) {
+  if (int st = ensure_slots(L)) return st;
   slot = L->next;
   L->next = (L->next + 1) % (int)L->slots.size();
   if (L->armed[slot]) {
@@ -140,12 +177,12 @@ int acquire(Loader* L, int& slot) {
 }
 
 void parallel_copy(Loader* L, void* dst, const void* src, uint64_t n) {
-  const int T = L->pool.size();
+  const int T = L->n_threads;
   if (n < (1u << 20) || T == 1) {
     std::memcpy(dst, src, n);
     return;
   }
-  L->pool.run([&](int w) {
+  pool(L).run([&](int w) {
     const uint64_t per = ((n + T - 1) / T + 63) & ~63ull;
     const uint64_t a = std::min<uint64_t>(n, per * w), b = std::min<uint64_t>(n, a + per);
     if (b > a) std::memcpy((char*)dst + a, (const char*)src + a, b - a);
@@ -159,21 +196,7 @@ extern "C" {
 void* rlk_loader_create(uint64_t slot_bytes, int n_slots, int n_threads) {
   if (slot_bytes == 0 || n_slots < 2) return nullptr;
   if (n_threads <= 0) n_threads = (int)std::max(1u, std::thread::hardware_concurrency());
-  auto* L = new Loader(slot_bytes, n_slots, n_threads);
-  for (int i = 0; i < n_slots; ++i) {
-    void* p = nullptr;
-    cudaEvent_t ev;
-    if (cudaHostAlloc(&p, slot_bytes, cudaHostAllocDefault) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
-      for (void* q : L->slots) cudaFreeHost(q);
-      delete L;
-      return nullptr;
-    }
-    L->slots.push_back(p);
-    L->events.push_back(ev);
-    L->armed.push_back(false);
-  }
-  return L;
+  return new Loader(slot_bytes, n_slots, n_threads);
 }
 
 void rlk_loader_destroy(void* ld) {
@@ -189,10 +212,28 @@ void rlk_loader_destroy(void* ld) {
 
 const char* rlk_loader_last_error(void) { return g_err; }
 
+// True when [p, p + bytes) is page-locked host memory the DMA engines can read directly.
+static bool host_pinned(const void* p, uint64_t bytes) {
+  if (!bytes) return false;
+  for (const char* q : {(const char*)p, (const char*)p + bytes - 1}) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+      cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+      return false;
+    }
+    if (at.type != cudaMemoryTypeHost) return false;
+  }
+  return true;
+}
+
 int rlk_loader_h2d(void* ld, void* dst_dev, const void* src_host, uint64_t bytes, void* stream) {
   auto* L = (Loader*)ld;
   if (!L || (!dst_dev && bytes) || (!src_host && bytes)) return RLK_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
+  if (host_pinned(src_host, bytes)) {
+    cudaError_t e = cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, s);
+    return e == cudaSuccess ? RLK_OK : fail("rlk_loader_h2d: cudaMemcpyAsync (pinned)", e);
+  }
   for (uint64_t off = 0; off < bytes; off += L->slot_bytes) {
     const uint64_t n = std::min<uint64_t>(L->slot_bytes, bytes - off);
     int slot;
@@ -210,7 +251,12 @@ int rlk_loader_d2h(void* ld, void* dst_host, const void* src_dev, uint64_t bytes
   auto* L = (Loader*)ld;
   if (!L || (bytes && (!dst_host || !src_dev))) return RLK_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
+  if (host_pinned(dst_host, bytes)) {
+    cudaError_t e = cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, s);
+    return e == cudaSuccess ? RLK_OK : fail("rlk_loader_d2h: cudaMemcpyAsync (pinned)", e);
+  }
   // issue all DMAs for a window of slots first, then drain them in order (copy-out overlaps DMA)
+  if (int st = ensure_slots(L)) return st;
   const int ns = (int)L->slots.size();
   std::vector<std::pair<int, uint64_t>> inflight;
   auto drain_one = [&]() -> int {
@@ -249,13 +295,13 @@ int rlk_loader_synth_h2d(void* ld, void* dst_dev, int dtype, uint64_t n, uint64_
   const uint64_t esz = dtype == RLK_BF16 ? 2 : 4;
   const uint64_t per_slot = L->slot_bytes / esz;
   cudaStream_t s = (cudaStream_t)stream;
-  const int T = L->pool.size();
+  const int T = L->n_threads;
   for (uint64_t e0 = 0; e0 < n; e0 += per_slot) {
     const uint64_t m = std::min<uint64_t>(per_slot, n - e0);
     int slot;
     if (int st = acquire(L, slot)) return st;
     void* buf = L->slots[slot];
-    L->pool.run([&](int w) {
+    pool(L).run([&](int w) {
       const uint64_t per = (m + T - 1) / T;
       const uint64_t a = std::min<uint64_t>(m, per * w), b = std::min<uint64_t>(m, a + per);
       for (uint64_t i = a; i < b; ++i) {
@@ -286,7 +332,8 @@ int rlk_loader_d2h_checksum(void* ld, const void* src_dev, uint64_t bytes, uint6
   if (!L || !checksum || (bytes && !src_dev) || (bytes & 7)) return RLK_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   std::atomic<uint64_t> acc{0};
-  const int T = L->pool.size();
+  const int T = L->n_threads;
+  if (int st = ensure_slots(L)) return st;
   const int ns = (int)L->slots.size();
   std::vector<std::pair<int, uint64_t>> inflight;
   auto drain_one = [&]() -> int {
@@ -297,7 +344,7 @@ int rlk_loader_d2h_checksum(void* ld, const void* src_dev, uint64_t bytes, uint6
     L->armed[slot] = false;
     const uint64_t words = std::min<uint64_t>(L->slot_bytes, bytes - off) / 8;
     const uint64_t* w64 = (const uint64_t*)L->slots[slot];
-    L->pool.run([&](int w) {
+    pool(L).run([&](int w) {
       const uint64_t per = (words + T - 1) / T;
       const uint64_t a = std::min<uint64_t>(words, per * w), b = std::min<uint64_t>(words, a + per);
       uint64_t local = 0;

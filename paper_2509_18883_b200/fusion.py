@@ -103,10 +103,10 @@ class FusionLayout:
     def n_tensors(self) -> int:
         return len(self.numels)
 
-    def tensor_items_device(self, device) -> torch.Tensor:
+    def tensor_items_device(self, device, stream=None) -> torch.Tensor:
         key = str(device)
         if key not in self._dev:
-            self._dev[key] = torch.from_numpy(self.tensor_items.astype(np.uint32).view(np.int32)).to(device)
+            self._dev[key] = _upload(self.tensor_items.astype(np.uint32).view(np.int32), device, stream)
         return self._dev[key]
 
     def partition(self, world: int, rank: int) -> list[tuple[int, int, int]]:
@@ -154,8 +154,18 @@ def _aligned(t: torch.Tensor) -> torch.Tensor:
     return t
 
 
+def _upload(arr: np.ndarray, device, stream=None) -> torch.Tensor:
+    """Small host table -> device.  With a stream: staged through pinned memory and copied
+    asynchronously on that stream (so it never waits behind bulk copies on another stream)."""
+    host = torch.from_numpy(np.ascontiguousarray(arr).copy())
+    if stream is None:
+        return host.to(device)
+    with torch.cuda.stream(stream):
+        return host.pin_memory().to(device, non_blocking=True)
+
+
 class _Plan:
-    def __init__(self, pieces: Sequence[Piece], layout: FusionLayout, n_experts: int, device):
+    def __init__(self, pieces: Sequence[Piece], layout: FusionLayout, n_experts: int, device, stream=None):
         segs = np.zeros(len(pieces), dtype=L.SEGMENT_DTYPE)
         counts = np.zeros(len(pieces), dtype=np.int64)
         for k, p in enumerate(pieces):
@@ -172,8 +182,8 @@ class _Plan:
             counts[k] = (p.numel + ITEM - 1) // ITEM
         prefix = np.zeros(len(pieces) + 1, dtype=np.uint32)
         np.cumsum(counts, out=prefix[1:])
-        self.segs_dev = torch.from_numpy(segs.view(np.uint8).copy()).to(device, non_blocking=False)
-        self.prefix_dev = torch.from_numpy(prefix.view(np.int32).copy()).to(device, non_blocking=False)
+        self.segs_dev = _upload(segs.view(np.uint8), device, stream)
+        self.prefix_dev = _upload(prefix.view(np.int32), device, stream)
         self.c = L.FusionPlanC(self.segs_dev.data_ptr(), self.prefix_dev.data_ptr(), len(pieces), int(prefix[-1]))
         self.max_extent = max((p.j0 + p.numel for p in pieces), default=0)
         self.local_elems = sum(p.numel for p in pieces)
@@ -187,7 +197,7 @@ class FusionCall:
 
     def __init__(self, pieces: Sequence[Piece], layout: FusionLayout, n_experts: int, cfg: FusionConfig,
                  *, delta_mode: bool = False, with_base: bool = True, group=None, stream=None,
-                 dropout_mode: int | None = None):
+                 dropout_mode: int | None = None, async_upload: bool = True):
         if not 1 <= n_experts <= L.RLK_MAX_EXPERTS:
             raise NotImplementedError(f"the B200 kernels fuse 1..{L.RLK_MAX_EXPERTS} experts, got {n_experts}")
         if not pieces:
@@ -202,7 +212,11 @@ class FusionCall:
         self.device = pieces[0].experts[0].device
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.dtype_in = pieces[0].experts[0].dtype
-        self.plan = _Plan(pieces, layout, n_experts, self.device)
+        # launch-plan tables go up on the call's stream (async) unless the caller builds plans while
+        # the device is idle (async_upload=False: one short blocking copy each)
+        up = stream if async_upload else None
+        self.plan = _Plan(pieces, layout, n_experts, self.device, up)
+        layout.tensor_items_device(self.device, up)
         nt = layout.n_tensors
         f64 = dict(dtype=torch.float64, device=self.device)
         self.sumsq = torch.empty((nt, n_experts), **f64)
@@ -282,7 +296,7 @@ class FusionCall:
                     from .dist import allreduce_partials
                     allreduce_partials(self.partials, self.group)
                 self._launch("rlk_fusion_finalize", L.ptr(self.partials),
-                       L.ptr(self.layout.tensor_items_device(self.device)), self.layout.n_tensors, self.n,
+                       L.ptr(self.layout.tensor_items_device(self.device, self.stream)), self.layout.n_tensors, self.n,
                        self.cfg.target_mode, float(self.cfg.target_norm) if self.cfg.target_mode == 2 else 0.0,
                        L.ptr(self.sumsq), L.ptr(self.scale), L.ptr(self.status), s)
             else:
@@ -318,11 +332,14 @@ class FusionCall:
                    L.ptr(self.bitmap), self.words_per_row, erase, L.ptr(self.counters), s)
         return self
 
-    def stats(self, tensor: int, weights: Sequence[float], size: int | None = None) -> FusionStats:
-        """FusionStats of one tensor (fusion.py:145-151, 165-182).  Synchronises."""
-        sumsq = self.sumsq[tensor].cpu().numpy()
-        scale = self.scale[tensor].cpu().numpy()
-        cnt = self.counters[tensor].cpu().numpy()
+    def stats(self, tensor: int, weights: Sequence[float], size: int | None = None,
+              host: tuple | None = None) -> FusionStats:
+        """FusionStats of one tensor (fusion.py:145-151, 165-182).  Synchronises (unless `host` holds
+        the (sumsq, scale, counters) tables already copied by `host_tables`)."""
+        if host is None:
+            sumsq, scale, cnt = (x[tensor].cpu().numpy() for x in (self.sumsq, self.scale, self.counters))
+        else:
+            sumsq, scale, cnt = (x[tensor] for x in host)
         size = self.layout.numels[tensor] if size is None else size
         norms = tuple(math.sqrt(float(x)) for x in sumsq)
         after = tuple(n if (self.cfg.target_norm is None or n == 0.0) else n * float(sc)
@@ -331,6 +348,10 @@ class FusionCall:
         kept = tuple(float(z) / size for z in nz)
         erased = tuple(int(e) for e in cnt[self.n:])
         return FusionStats(norms, after, kept, erased, tuple(float(x) for x in weights))
+
+    def host_tables(self) -> tuple:
+        """(sumsq, scale, counters) as host arrays, one copy each (for stats over many tensors)."""
+        return tuple(x.cpu().numpy() for x in (self.sumsq, self.scale, self.counters))
 
 
 # ----------------------------------------------------------------------------- task vectors

@@ -29,7 +29,7 @@ class HostLoader:
     def __init__(self, slot_bytes: int = 64 << 20, n_slots: int = 4, n_threads: int = 0):
         self._h = L.lib().rlk_loader_create(slot_bytes, n_slots, n_threads)
         if not self._h:
-            raise L.RlkError("rlk_loader_create failed (pinned allocation)")
+            raise L.RlkError("rlk_loader_create failed (slot_bytes must be > 0 and n_slots >= 2)")
 
     def _check(self, st: int, what: str) -> None:
         if st != 0:
@@ -136,14 +136,13 @@ class StreamingReport:
 
 
 def plan_groups(numels: Sequence[int], n_experts: int, esize: int, budget_bytes: int) -> list[list[int]]:
-    """Consecutive tensor groups whose (N+1 inputs + output) bytes fit half the budget each."""
-    half = budget_bytes // 2
+    """Consecutive tensor groups whose (N+1 inputs + output) bytes fit `budget_bytes` each."""
     groups, cur, cur_b = [], [], 0
     for t, n in enumerate(numels):
-        b = (n + 63) // 64 * 64 * esize * (n_experts + 2)
-        if b > half:
-            raise ValueError(f"tensor {t} ({n} elements) does not fit half the device budget; raise the budget")
-        if cur and cur_b + b > half:
+        b = _footprint(n, n_experts, esize)
+        if b > budget_bytes:
+            raise ValueError(f"tensor {t} ({n} elements) does not fit the workspace; raise the budget")
+        if cur and cur_b + b > budget_bytes:
             groups.append(cur)
             cur, cur_b = [], 0
         cur.append(t)
@@ -153,66 +152,109 @@ def plan_groups(numels: Sequence[int], n_experts: int, esize: int, budget_bytes:
     return groups
 
 
+def _footprint(n: int, n_experts: int, esize: int) -> int:
+    return (n + 63) // 64 * 64 * esize * (n_experts + 2)
+
+
 def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, source, sink,
                    cfg: FusionConfig = FusionConfig(), dtype: torch.dtype = torch.bfloat16,
                    device_budget_bytes: int = 64 << 30, stats: bool = True,
-                   loader: HostLoader | None = None) -> StreamingReport:
-    """Fuse a host-resident (or synthesised) checkpoint through the device in double-buffered groups."""
+                   loader: HostLoader | None = None, group_bytes: int = 2 << 30) -> StreamingReport:
+    """Fuse a host-resident (or synthesised) checkpoint through the device in pipelined groups.
+
+    Consecutive tensors are grouped up to min(`group_bytes`, half the budget) of device footprint
+    ((N+1) inputs + output; a larger tensor is a group of its own) and placed one after another in a ring buffer of
+    `device_budget_bytes`.  Three streams: H2D of group g + 1, the fusion kernels of group g and the
+    D2H of group g - 1 run concurrently (PCIe is full duplex); a group's H2D waits (on events, not on
+    the host) for the D2H of every earlier group whose ring space it reuses.  Pinned host
+    sources/sinks are DMA'd directly; pageable ones go through the loader's pinned slots."""
     dev = torch.device("cuda", torch.cuda.current_device())
     esize = torch.tensor([], dtype=dtype).element_size()
-    groups = plan_groups(numels, n_experts, esize, device_budget_bytes)
+    cap = device_budget_bytes // esize // 64 * 64  # ring capacity in elements
+    biggest = max(_footprint(n, n_experts, esize) for n in numels) // esize
+    if biggest > cap:
+        raise ValueError("the largest tensor does not fit the device budget; raise the budget")
+    # groups of at most half the ring, so that one can stream in while the previous one computes
+    groups = plan_groups(numels, n_experts, esize, max(min(group_bytes, device_budget_bytes // 2), biggest * esize))
+    # ring placement, decided up front: offset of each group and the earlier groups it overwrites
+    place, waits, live, head = [], [], [], 0
+    for gi, group in enumerate(groups):
+        size = sum(_footprint(numels[t], n_experts, esize) for t in group) // esize
+        if head + size > cap:
+            head = 0
+        lo, hi = head, head + size
+        waits.append([j for j, a, b in live if a < hi and lo < b])
+        live = [(j, a, b) for j, a, b in live if not (a < hi and lo < b)] + [(gi, lo, hi)]
+        place.append(lo)
+        head = hi
+    ring = torch.empty(min(cap, max(p + sum(_footprint(numels[t], n_experts, esize) for t in g) // esize
+                                    for p, g in zip(place, groups))), dtype=dtype, device=dev)
     own_loader = loader is None
     loader = loader or HostLoader()
-    copy_s, comp_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    h2d_s, comp_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     weights = cfg.merge_weights or tuple(1.0 / n_experts for _ in range(n_experts))
-    half_elems = (device_budget_bytes // 2) // esize
-    # two workspaces, each one flat buffer carved per group: (N+1) inputs + output
-    ws = [torch.empty(half_elems, dtype=dtype, device=dev) for _ in range(2)]
     rep = StreamingReport(groups=len(groups))
-    pending = None  # (names, out views, compute-done event, call, tensor ids)
+
+    def build(gi, group):
+        off = place[gi]
+        pieces, views_all = [], []
+        for k, t in enumerate(group):
+            n = numels[t]
+            views = []
+            for _ in range(n_experts + 2):
+                views.append(ring[off:off + n])
+                off += (n + 63) // 64 * 64  # keep 128-byte alignment
+            pieces.append(Piece(k, 0, views[0], views[1:n_experts + 1], views[-1]))
+            views_all.append(views)
+        layout = FusionLayout([numels[t] for t in group])
+        return group, views_all, FusionCall(pieces, layout, n_experts, cfg, stream=comp_s, async_upload=False)
+
+    # every launch plan is built before the first bulk copy: its small blocking uploads must not queue
+    # behind gigabytes of H2D traffic (and pinned staging for them would not recycle in time)
+    plans = [build(gi, group) for gi, group in enumerate(groups)]
+    freed: dict[int, torch.cuda.Event] = {}  # group -> its D2H has completed
+    pending = None  # (group index, out views, compute-done event)
     try:
-        for gi, group in enumerate(groups):
-            buf = ws[gi % 2]
-            # the previous user of this workspace must have drained (its D2H ran on copy_s, in order)
-            off = 0
-            pieces, outs = [], []
-            for k, t in enumerate(group):
-                n = numels[t]
-                views = []
-                for _ in range(n_experts + 2):
-                    views.append(buf[off:off + n])
-                    off += (n + 63) // 64 * 64  # keep 128-byte alignment
+        for gi, (group, views_all, call) in enumerate(plans):
+            for j in waits[gi]:
+                if pending is not None and pending[0] == j:  # ring too small to overlap: drain now
+                    freed[j] = _drain(pending, loader, sink, d2h_s, names, rep, groups)
+                    pending = None
+                h2d_s.wait_event(freed.pop(j))
+            for t, views in zip(group, views_all):
                 for si in range(n_experts + 1):
-                    source.fill(loader, names[t], si, views[si], copy_s)
-                    rep.h2d_bytes += n * esize
-                pieces.append(Piece(k, 0, views[0], views[1:n_experts + 1], views[-1]))
-                outs.append(views[-1])
+                    source.fill(loader, names[t], si, views[si], h2d_s)
+                    rep.h2d_bytes += numels[t] * esize
             ready = torch.cuda.Event()
-            ready.record(copy_s)
+            ready.record(h2d_s)
             comp_s.wait_event(ready)
-            call = FusionCall(pieces, FusionLayout([numels[t] for t in group]), n_experts, cfg, stream=comp_s)
             call.run(weights)
             done = torch.cuda.Event()
             done.record(comp_s)
             # drain the previous group while this one computes
             if pending is not None:
-                _drain(pending, loader, sink, copy_s, names, rep, stats, weights)
-            pending = (group, outs, done, call)
+                freed[pending[0]] = _drain(pending, loader, sink, d2h_s, names, rep, groups)
+            pending = (gi, [v[-1] for v in views_all], done)
         if pending is not None:
-            _drain(pending, loader, sink, copy_s, names, rep, stats, weights)
+            _drain(pending, loader, sink, d2h_s, names, rep, groups)
         torch.cuda.synchronize(dev)
+        if stats:
+            for group, _, call in plans:
+                host = call.host_tables()
+                for k, t in enumerate(group):
+                    rep.stats[names[t]] = call.stats(k, weights, host=host)
     finally:
         if own_loader:
             loader.close()
     return rep
 
 
-def _drain(pending, loader, sink, copy_s, names, rep, stats, weights):
-    group, outs, done, call = pending
-    copy_s.wait_event(done)
-    for t, o in zip(group, outs):
-        sink.drain(loader, names[t], o, copy_s)
+def _drain(pending, loader, sink, d2h_s, names, rep, groups) -> torch.cuda.Event:
+    gi, outs, done = pending
+    d2h_s.wait_event(done)
+    for t, o in zip(groups[gi], outs):
+        sink.drain(loader, names[t], o, d2h_s)
         rep.d2h_bytes += o.numel() * o.element_size()
-    if stats:
-        for k, t in enumerate(group):
-            rep.stats[names[t]] = call.stats(k, weights)
+    ev = torch.cuda.Event()
+    ev.record(d2h_s)
+    return ev

@@ -40,6 +40,31 @@ def test_streaming_equals_in_hbm(cuda, budget):
         assert list(rep.stats[k].dropout_kept_fraction) == st["kept"]
 
 
+@pytest.mark.parametrize("pinned,budget", [(False, 32 << 20), (True, 32 << 20), (True, 2 << 20)])
+def test_streaming_ring_of_workspaces(cuda, pinned, budget):
+    """Many small groups through the device ring buffer, pageable or pinned host buffers (the pinned
+    path DMAs directly); a 2 MiB ring forces every group to wait for its predecessor's D2H.  Identical
+    to the all-in-HBM fuse."""
+    from paper_2509_18883_b200 import fusion as F
+    from paper_2509_18883_b200.loader import ArraySink, ArraySource, fuse_streaming
+    shapes = {f"t{i}": (257 + 64 * i, 129) for i in range(20)}
+    base, experts = synth_state_dicts(shapes, 3, seed=17, dtype_round=bf16_round)
+    pin = (lambda t: t.pin_memory()) if pinned else (lambda t: t)
+    hb = {k: pin(v) for k, v in _host_bf16(base).items()}
+    he = [{k: pin(v) for k, v in _host_bf16(e).items()} for e in experts]
+    out = {k: pin(torch.empty(v.shape, dtype=torch.bfloat16)) for k, v in hb.items()}
+    names = list(hb)
+    cfg = F.FusionConfig(dropout_p=0.3, seed=1)
+    rep = fuse_streaming(names, [hb[k].numel() for k in names], 3, ArraySource(hb, he), ArraySink(out), cfg,
+                         device_budget_bytes=budget, group_bytes=2 << 20)
+    assert rep.groups >= 8
+    dev_out, drep = F.fuse_state_dict({k: v.to(cuda) for k, v in hb.items()},
+                                      [{k: v.to(cuda) for k, v in e.items()} for e in he], cfg)
+    for k in names:
+        assert torch.equal(out[k].view(torch.int16), dev_out[k].cpu().view(torch.int16)), k
+        assert rep.stats[k].erased_counts == drep.stats(k).erased_counts, k
+
+
 def test_loader_roundtrip_and_checksum(cuda):
     from paper_2509_18883_b200.loader import HostLoader
     ld = HostLoader(slot_bytes=1 << 20, n_slots=4, n_threads=3)
@@ -50,6 +75,14 @@ def test_loader_roundtrip_and_checksum(cuda):
     back = np.empty_like(src)
     ld.d2h(back, dst, s)
     assert np.array_equal(back, src)
+    # page-locked host buffers take the direct DMA path
+    src_p = torch.from_numpy(src.view(np.int16)).pin_memory()
+    dst2 = torch.empty_like(dst)
+    ld.h2d(dst2, src_p, s)
+    back_p = torch.empty_like(src_p).pin_memory()
+    ld.d2h(back_p, dst2, s)
+    s.synchronize()
+    assert np.array_equal(back_p.numpy().view(np.uint16), src)
     x = torch.arange(1 << 20, dtype=torch.int64, device=cuda)
     torch.cuda.synchronize()  # produced on the default stream, read on s
     assert ld.d2h_checksum(x.view(torch.uint8), s) == sum(range(1 << 20))
