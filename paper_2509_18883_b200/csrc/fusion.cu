@@ -421,10 +421,26 @@ __global__ void k_finalize(const double* __restrict__ partials, const uint32_t* 
 }
 
 // ------------------------------------------------------------------ K2: dropout keep bitmap
+// High word of mix64(z) (core.py:42-49) with the second product computed for its high word only:
+// hi32(z * K2 mod 2^64) = hi32(lo * K2lo) + lo * K2hi + hi * K2lo (mod 2^32); the final
+// z ^= z >> 31 changes the high word to h ^ (h >> 31).
+__device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
+  z ^= z >> 30;
+  z *= kMix1;
+  z ^= z >> 27;
+  const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+  const uint32_t h = __umulhi(lo, (uint32_t)kMix2) + lo * (uint32_t)(kMix2 >> 32) + hi * (uint32_t)kMix2;
+  return h ^ (h >> 31);
+}
+
+// HI: thresh << 11 has a zero low word (e.g. p = 0.5), so keep <=> high word of the draw >= its high
+// word -- exact, and the low word of the draw is never needed.
+template <bool HI>
 __global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, uint64_t thresh, uint64_t n_bits,
                               uint32_t* __restrict__ bitmap, uint64_t words_per_row) {
   // keep iff (mix64(c_j) >> 11) >= thresh  <=>  mix64(c_j) >= thresh << 11  (thresh <= 2^53)
   const uint64_t t64 = thresh << 11;
+  const uint32_t t_hi = (uint32_t)(t64 >> 32);
   const bool all = thresh == 0;  // p == 0: every draw kept (t64 == 0)
   const uint64_t words = (n_bits + 31) / 32;
   const int i = blockIdx.y;  // expert (grid.y = N): no 64-bit division per word
@@ -435,7 +451,8 @@ __global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, u
     uint64_t c = seed + (w * 32 + 1) * kGamma;  // counter of draw j = 32 w (core.py:69-71)
 #pragma unroll 8
     for (int b = 0; b < 32; ++b) {
-      bits |= (uint32_t)(all || mix64(c) >= t64) << b;
+      const bool keep = HI ? mix64_hi(c) >= t_hi : mix64(c) >= t64;
+      bits |= (uint32_t)(all || keep) << b;
       c += kGamma;
     }
     bitmap[(uint64_t)i * words_per_row + w] = bits;
@@ -1177,8 +1194,8 @@ int rlk_fusion_mask_bitmap(const uint64_t* child_seeds, int n_experts, uint64_t 
   const uint64_t words = (n_bits + 31) / 32;
   const uint64_t blocks = (words + 255) / 256;
   const uint32_t gx = (uint32_t)std::min<uint64_t>(blocks, (uint64_t)sm_count() * 16 / n_experts + 1);
-  k_mask_bitmap<<<dim3(gx, n_experts), 256, 0, (cudaStream_t)stream>>>(lo, hi, n_experts, thresh, n_bits, bitmap,
-                                                                    words_per_row);
+  auto kern = ((thresh << 11) & 0xffffffffull) == 0 ? k_mask_bitmap<true> : k_mask_bitmap<false>;
+  kern<<<dim3(gx, n_experts), 256, 0, (cudaStream_t)stream>>>(lo, hi, n_experts, thresh, n_bits, bitmap, words_per_row);
   return launch_status("rlk_fusion_mask_bitmap");
 }
 
