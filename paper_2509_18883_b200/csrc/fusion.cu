@@ -726,6 +726,15 @@ __device__ __forceinline__ uint32_t select_halves(uint32_t x, uint32_t b, uint32
   asm("lop3.b32 %0, %1, %2, %3, 0xe4;" : "=r"(r) : "r"(x), "r"(b), "r"(m));
   return r;
 }
+// (lo, hi) bf16 halves of w minus the f32 pair b, each rounded once to f32 (sub.rn.f32.bf16: one
+// FHADD.BF16 per element reading the bf16 half in place -- no unpacking)
+__device__ __forceinline__ float2 bf16x2_minus_f32(uint32_t w, float2 b) {
+  float2 r;
+  asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n sub.rn.f32.bf16 %0, lo, %3;\n sub.rn.f32.bf16 %1, hi, %4;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(w), "f"(b.x), "f"(b.y));
+  return r;
+}
 // +-1.0f with the sign of x (one LOP3)
 __device__ __forceinline__ float sign_one(float x) {
   uint32_t r;
@@ -860,7 +869,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
           for (int i = 0; i < N; ++i) {
             uint32_t xw = xw4[i].w[p];
             if (DROP) xw = select_halves(xw, bw, prmt_sign(spread[i], p == 0 ? 0x9988u : 0xBBAAu));
-            const float2 d2 = __ffma2_rn(b2, make_float2(-1.f, -1.f), make_float2(bf16_lo(xw), bf16_hi(xw)));
+            const float2 d2 = bf16x2_minus_f32(xw, b2);
             k2[i] = __fmul2_rn(d2, make_float2(sr32[i], sr32[i]));
             aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
           }
