@@ -326,12 +326,16 @@ __global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd(FwdArgs a) {
 // K4a streams every row and leaves per-(row, warp) partials (max z, sum 2^((z - max) c)) in a
 // workspace -- no block-level synchronisation anywhere in the streaming loop; K4b combines the
 // kGW partials of a row in f64 and runs the epilogue, one thread per row.
+#ifndef RLK_K4A_CTAS
+#define RLK_K4A_CTAS 2
+#endif
+constexpr int kK4aCtas = RLK_K4A_CTAS;  // CTAs per SM of the streaming forward (ring split between them)
 template <int DT>
-__global__ void __launch_bounds__(kGThreads, 1) k_grpo_fwd_stream(FwdArgs a, float* __restrict__ ws) {
+__global__ void __launch_bounds__(kGThreads, kK4aCtas) k_grpo_fwd_stream(FwdArgs a, float* __restrict__ ws) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DT>::size;
   constexpr int VEC = 16 / ESZ;
-  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages, kGW);
+  const Ring r = ring_setup(smem, kRowStageBytes, kRowStages / kK4aCtas, kGW);
   const uint64_t row_bytes = a.vocab * ESZ;
   auto active = [&](uint64_t row) { return a.use[a.sample[row]] != 0; };
   auto addr = [&](uint64_t row) {
@@ -742,10 +746,11 @@ static int set_smem(K kern, uint32_t bytes) {
 
 template <int DT>
 static int launch_fwd_split(const FwdArgs& a, float* ws, cudaStream_t s) {
-  const uint32_t smem = 1024 + kRowStageBytes * kRowStages;
+  const uint32_t smem = 1024 + kRowStageBytes * (kRowStages / kK4aCtas);
   auto kern = k_grpo_fwd_stream<DT>;
   if (int st = set_smem(kern, smem)) return st;
-  kern<<<grid_rows(a.n_rows), kGThreads, smem, s>>>(a, ws);
+  const uint64_t ctas = (uint64_t)sm_count() * kK4aCtas;
+  kern<<<(unsigned)(a.n_rows < ctas ? a.n_rows : ctas), kGThreads, smem, s>>>(a, ws);
   if (int st = launch_status("rlk_grpo_fwd (stream)")) return st;
   const uint64_t blocks = (a.n_rows + 255) / 256;
   k_grpo_fwd_epilogue<DT><<<(unsigned)std::min<uint64_t>(blocks, 65535u * 16), 256, 0, s>>>(a, ws);
