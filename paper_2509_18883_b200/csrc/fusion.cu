@@ -56,7 +56,11 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
   constexpr uint32_t ELEMS = SB / ESZ;
   constexpr uint32_t BMB = ELEMS / 8;  // bitmap bytes per expert per full stage
   const int ns = with_base ? N + 1 : N;
+  // parameter streams are read once (evict_first); every tensor re-reads the keep-bitmap prefix
+  // [0, numel) of each expert row, so the bitmap is kept in L2 (evict_last): the prefixes of all but
+  // the embedding-sized tensors fit, and their re-reads stop costing HBM traffic
   const uint64_t pol = policy_evict_first();
+  const uint64_t pol_bm = policy_evict_last();
   RingPos q;
   for (uint32_t item = blockIdx.x; item < plan.n_items; item += gridDim.x) {
     const ItemGeom g = item_geom(plan, item);
@@ -88,7 +92,7 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
           const uint64_t jb = jtensor0 + off;  // multiple of ELEMS -> byte offset multiple of 16
           for (int i = 0; i < N; ++i)
             bulk_g2s(dst + (N + 1) * SB + i * BMB, (const char*)(bitmap + i * words_per_row) + jb / 8, bm_bytes,
-                     &r.full[s], pol);
+                     &r.full[s], pol_bm);
         }
       } else {
         mbar_arrive(&r.full[s]);
