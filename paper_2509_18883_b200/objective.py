@@ -372,6 +372,27 @@ def token_logprobs(logits2d: torch.Tensor, tokens: Sequence[int], temperature: f
 
 
 # ----------------------------------------------------------------------------- object API (reference)
+class _LogDistCache:
+    """Memoizes per-(context, position, temperature) log-dists for one call (objective.py:206-220).
+
+    The batched paths (objective_value / objective_gradient) compute every row's log-sum-exp in one
+    K4 launch instead; this mirror serves callers of the reference's per-token interface, each miss
+    being one device row (`toy_env.log_token_dist`, the fused log-softmax kernel)."""
+
+    def __init__(self, params: ParamTable):
+        from .toy_env import TrainEngine
+        self.params = params
+        self.engine = TrainEngine()
+        self._cache: dict[tuple[int, int, float], torch.Tensor] = {}
+
+    def get(self, context_id: int, position: int, temperature: float) -> torch.Tensor:
+        from .toy_env import log_token_dist
+        key = (context_id, position, temperature)
+        if key not in self._cache:
+            self._cache[key] = log_token_dist(self.params, self.engine, context_id, position, temperature)
+        return self._cache[key]
+
+
 def _require_logps(sample: Sample) -> None:
     if sample.train_logps is None:
         raise ValueError(f"sample for prompt {sample.prompt_id} is missing train log-probs")

@@ -159,6 +159,12 @@ def test_log_token_dist_and_trace(cuda):
     np.testing.assert_allclose(tr, ref, rtol=1e-13)
     with pytest.raises(IndexError):
         log_token_dist(pt, TrainEngine(), 2, 0)
+    # the reference's per-call memo (objective.py:206-220): same rows, computed once per key
+    from paper_2509_18883_b200 import objective as O
+    cache = O._LogDistCache(pt)
+    a = cache.get(1, 2, 0.6)
+    assert cache.get(1, 2, 0.6) is a and len(cache._cache) == 1
+    np.testing.assert_allclose(a.cpu().numpy(), OO.log_token_dist(logits[1, 2], 0.6), rtol=1e-13, atol=1e-14)
 
 
 def test_bad_token_flag(cuda):
