@@ -46,6 +46,11 @@ def label_hash(label: RngLabel) -> int:
     return h
 
 
+# the reference's private names (core.py:42, 52), for callers that import them
+_mix64 = mix64
+_label_hash = label_hash
+
+
 class Rng:
     """Counter-based SplitMix64 stream (core.py:60-97); `split` derives children from the seed only."""
 
