@@ -163,6 +163,16 @@ __device__ __forceinline__ void warp_combine(float& mz, float& sum, float c, uns
   }
 }
 
+// Per-row operands the consumers need, published in shared memory by the epilogue warp one row ahead
+// (so the dependent global loads sample -> use / temperature never sit on the consumers' path).
+struct RowInfo {
+  uint64_t row;   // next active row (>= n_rows: none)
+  uint64_t lrow;  // its logits / grad row (row_index)
+  float c;        // log2(e) / temperature
+  int32_t tok;    // target token
+};
+static_assert(896 + 2 * sizeof(RowInfo) <= 1024, "RowInfo must fit the 1 KiB header");
+
 // Warp roles: 16 consumer warps (both passes), one producer warp (lane 0 issues TMA), one epilogue
 // warp.  Rows are software-pipelined: after pass 1 of row r the consumers hand their partials to the
 // epilogue warp (mbarrier), run pass 1 over the chunks of the next row that are already in the ring,
@@ -170,8 +180,8 @@ __device__ __forceinline__ void warp_combine(float& mz, float& sum, float c, uns
 // serial epilogue are off the consumers' critical path.
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo_fused_bf16(FusedArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  // 1 KiB header: [full[nslots] | empty[nslots] | xbar[2] | pready[2] | cready[2]] (<= 512 B),
-  // slot[2] float2 @512, bcast[2][4] float @576, red[2][kFW][2] float @640
+  // 1 KiB header: [full[nslots] | empty[nslots] | xbar[2] | pready[2] | cready[2] | ibar[2]] (<= 512 B),
+  // slot[2] float2 @512, bcast[2][4] float @576, red[2][kFW][2] float @640, info[2] RowInfo @896
   const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
   const uint64_t half = a.vocab / 2;  // elements owned by this CTA (vocab % 16 == 0)
   const uint64_t v0 = rank * half;
@@ -184,7 +194,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
   uint64_t* xbar = empty + nslots;
   uint64_t* pready = xbar + 2;
   uint64_t* cready = pready + 2;
+  uint64_t* ibar = cready + 2;
   float2* slot = reinterpret_cast<float2*>(smem + 512);
+  RowInfo* info = reinterpret_cast<RowInfo*>(smem + 896);
   float* bcast = reinterpret_cast<float*>(smem + 576);
   float* red = reinterpret_cast<float*>(smem + 640);
   uint8_t* buf = smem + 1024;
@@ -198,6 +210,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       mbar_init(&xbar[k], 1);
       mbar_init(&pready[k], kFW);
       mbar_init(&cready[k], 1);
+      mbar_init(&ibar[k], 1);
     }
     fence_mbar_init();
   }
@@ -232,6 +245,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
     for (uint64_t row = row0; row < a.n_rows; row += rstep) {
       if (!active(row)) continue;
       const uint32_t p = (uint32_t)(it++ & 1u);
+      if (lane == 0) {
+        // the consumers read this after pass 1 of `row` (ibar[p] completes once per use of parity p;
+        // info[p] of two rows back was consumed before pass 2 of the previous row started)
+        uint64_t nr = row + rstep;
+        while (nr < a.n_rows && !active(nr)) nr += rstep;
+        RowInfo ni;
+        ni.row = nr;
+        ni.lrow = 0;
+        ni.c = 0.f;
+        ni.tok = 0;
+        if (nr < a.n_rows) {
+          ni.lrow = lrow(nr);
+          ni.c = (float)(kLog2eF / a.temp[a.sample[nr]]);
+          ni.tok = a.tokens[nr];
+        }
+        info[p] = ni;
+        mbar_arrive(&ibar[p]);
+      }
       const int32_t s_id = a.sample[row];
       const double T = a.temp[s_id];
       const float c = (float)(kLog2eF / T);
@@ -306,26 +337,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
     RowAcc acc;
     acc.reset();
     uint32_t done = 0;  // chunks of the current row already reduced by the previous iteration's pre-pass
-    auto next_active = [&](uint64_t row) {
-      // zero the gradient of inactive rows on the way (objective.py:240-241 / 275-276)
-      for (; row < a.n_rows; row += rstep) {
-        if (active(row)) return row;
-        uint16_t* grow = a.grad + lrow(row) * a.grad_row_stride + v0;
-        for (uint64_t b = (uint64_t)tid * 8; b < half; b += (uint64_t)kFT * 8) stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
-        if (rank == 0 && tid == 0) {
-          if (a.logp) a.logp[row] = 0.0;
-          if (a.lse) a.lse[row] = 0.0;
-          a.term[row] = 0.0;
-          a.coef[row] = 0.0;
-        }
+    uint32_t iph[2] = {0u, 0u};
+    // zero the gradient and outputs of inactive rows (objective.py:240-241 / 275-276)
+    auto zero_row = [&](uint64_t row) {
+      uint16_t* grow = a.grad + lrow(row) * a.grad_row_stride + v0;
+      for (uint64_t b = (uint64_t)tid * 8; b < half; b += (uint64_t)kFT * 8) stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
+      if (rank == 0 && tid == 0) {
+        if (a.logp) a.logp[row] = 0.0;
+        if (a.lse) a.lse[row] = 0.0;
+        a.term[row] = 0.0;
+        a.coef[row] = 0.0;
       }
-      return row;
     };
-    uint64_t row = next_active(row0);
+    uint64_t row = row0;
+    for (; row < a.n_rows && !active(row); row += rstep) zero_row(row);
+    float c = 0.f;
+    int32_t tok = 0;
+    uint64_t lr = 0;
+    if (row < a.n_rows) {
+      c = (float)(kLog2eF / a.temp[a.sample[row]]);
+      tok = a.tokens[row];
+      lr = lrow(row);
+    }
     RingPos q_row = q;  // ring position of the current row's chunk 0
     while (row < a.n_rows) {
       const uint32_t p = (uint32_t)(it++ & 1u);
-      const float c = (float)(kLog2eF / a.temp[a.sample[row]]);
       // pass 1 (rest of the row)
       for (uint32_t k = done; k < nch; ++k) {
         mbar_wait(&full[q.s], q.ph);
@@ -340,12 +376,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         mbar_arrive(&pready[p]);
       }
       // pass 1 of the next active row over the chunks already in the ring
-      const uint64_t nrow = next_active(row + rstep);
+      mbar_wait(&ibar[p], iph[p]);
+      iph[p] ^= 1u;
+      const RowInfo ni = info[p];
+      const uint64_t nrow = ni.row;
+      for (uint64_t zr = row + rstep; zr < nrow && zr < a.n_rows; zr += rstep) zero_row(zr);
       const RingPos q_next = q;
       acc.reset();
       done = 0;
       if (nrow < a.n_rows) {
-        const float cn = (float)(kLog2eF / a.temp[a.sample[nrow]]);
+        const float cn = ni.c;
         for (; done < pre; ++done) {
           mbar_wait(&full[q.s], q.ph);
           acc.chunk(buf + q.s * kChunkBytes, min(kChunkBytes, half_bytes - done * kChunkBytes), cn, tid);
@@ -356,9 +396,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       mbar_wait(&cready[p], cph[p]);
       cph[p] ^= 1u;
       const float cf = bcast[p * 4 + 0], nl = bcast[p * 4 + 1];
-      uint16_t* grow = a.grad + lrow(row) * a.grad_row_stride + v0;
+      uint16_t* grow = a.grad + lr * a.grad_row_stride + v0;
       // the chunk / vector / thread that holds the target token's logit (the one-hot term)
-      const int64_t tok_local = (int64_t)a.tokens[row] - (int64_t)v0;
+      const int64_t tok_local = (int64_t)tok - (int64_t)v0;
       const bool tok_here = tok_local >= 0 && tok_local < (int64_t)half;
       const uint32_t tok_chunk = tok_here ? (uint32_t)(tok_local / (kChunkBytes / 2)) : 0xffffffffu;
       const uint32_t tok_vec = tok_here ? (uint32_t)(tok_local % (kChunkBytes / 2)) / 8 : 0u;
@@ -388,6 +428,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         q2.next(nslots);
       }
       row = nrow;
+      c = ni.c;
+      tok = ni.tok;
+      lr = ni.lrow;
       q_row = q_next;
     }
   }
