@@ -12,6 +12,7 @@
  *                           ParamTable finite check                  toy_env.py:67-72
  *   rlk_fusion_finalize     normalize_magnitudes target/scale        fusion.py:86-102
  *   rlk_fusion_mask_bitmap  dropout_prune draw loop                  fusion.py:105-115, core.py:69-75, 95-103
+ *   rlk_fusion_mask_bitmap_range  (the same, one index slice)       fusion.py:105-115
  *   rlk_fusion_merge        dropout_prune rescale, erase_minority,   fusion.py:114, 118-142
  *                           fuse weighted sum + FusionStats counts   fusion.py:154-188
  *   rlk_grpo_fwd            log_token_dist + objective_value         toy_env.py:157-175, objective.py:230-250
@@ -97,6 +98,11 @@ int rlk_fusion_finalize(const double* partials, const uint32_t* tensor_items, ui
  * (mix64(child_seeds[i] + (j+1)*0x9E3779B97F4A7C15) >> 11) >= thresh.  child_seeds is a HOST array. */
 int rlk_fusion_mask_bitmap(const uint64_t* child_seeds, int n_experts, uint64_t thresh, uint64_t n_bits,
                            uint32_t* bitmap, uint64_t words_per_row, void* stream);
+/* The same bits for indices [bit_lo, bit_hi) only (bit_lo % 32 == 0): a sharded job draws its slice of
+ * the rows and all-gathers them (FusionCall under a process group) instead of every rank drawing
+ * every row. */
+int rlk_fusion_mask_bitmap_range(const uint64_t* child_seeds, int n_experts, uint64_t thresh, uint64_t bit_lo,
+                                 uint64_t bit_hi, uint32_t* bitmap, uint64_t words_per_row, void* stream);
 
 /* K3 merge.  delta_mode: 0 = experts are expert tables (delta = expert - base); bit 0 set = experts are
  * task-vector deltas, and then bit 1 says whether the base stream is present (fused = base + sum) or

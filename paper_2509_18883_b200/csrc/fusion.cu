@@ -440,8 +440,8 @@ __device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
 // HI: thresh << 11 has a zero low word (e.g. p = 0.5), so keep <=> high word of the draw >= its high
 // word -- exact, and the low word of the draw is never needed.
 template <bool HI>
-__global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, uint64_t thresh, uint64_t n_bits,
-                              uint32_t* __restrict__ bitmap, uint64_t words_per_row) {
+__global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, uint64_t thresh, uint64_t w_lo,
+                              uint64_t n_bits, uint32_t* __restrict__ bitmap, uint64_t words_per_row) {
   // keep iff (mix64(c_j) >> 11) >= thresh  <=>  mix64(c_j) >= thresh << 11  (thresh <= 2^53)
   const uint64_t t64 = thresh << 11;
   const uint32_t t_hi = (uint32_t)(t64 >> 32);
@@ -450,7 +450,7 @@ __global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, u
   const int i = blockIdx.y;  // expert (grid.y = N): no 64-bit division per word
   const uint64_t seed = i < 4 ? (&seeds_lo.x)[i] : (&seeds_hi.x)[i - 4];
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += stride) {
+  for (uint64_t w = w_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += stride) {
     uint32_t bits = 0;
     uint64_t c = seed + (w * 32 + 1) * kGamma;  // counter of draw j = 32 w (core.py:69-71)
 #pragma unroll 8
@@ -1195,21 +1195,28 @@ int rlk_fusion_finalize(const double* partials, const uint32_t* tensor_items, ui
   return launch_status("rlk_fusion_finalize");
 }
 
-int rlk_fusion_mask_bitmap(const uint64_t* child_seeds, int n_experts, uint64_t thresh, uint64_t n_bits,
-                           uint32_t* bitmap, uint64_t words_per_row, void* stream) {
+int rlk_fusion_mask_bitmap_range(const uint64_t* child_seeds, int n_experts, uint64_t thresh, uint64_t bit_lo,
+                                 uint64_t bit_hi, uint32_t* bitmap, uint64_t words_per_row, void* stream) {
   RLK_REQUIRE(n_experts >= 1 && n_experts <= RLK_MAX_EXPERTS, "rlk_fusion_mask_bitmap: bad expert count %d",
               n_experts);
   RLK_REQUIRE(child_seeds && bitmap, "rlk_fusion_mask_bitmap: NULL argument");
-  RLK_REQUIRE(words_per_row * 32 >= n_bits, "rlk_fusion_mask_bitmap: row too short");
-  if (n_bits == 0) return RLK_OK;
+  RLK_REQUIRE(bit_lo % 32 == 0 && bit_lo <= bit_hi, "rlk_fusion_mask_bitmap: bad bit range");
+  RLK_REQUIRE(words_per_row * 32 >= bit_hi, "rlk_fusion_mask_bitmap: row too short");
+  if (bit_hi == bit_lo) return RLK_OK;
   ulonglong4 lo = make_ulonglong4(0, 0, 0, 0), hi = make_ulonglong4(0, 0, 0, 0);
   for (int i = 0; i < n_experts; ++i) (i < 4 ? (&lo.x)[i] : (&hi.x)[i - 4]) = child_seeds[i];
-  const uint64_t words = (n_bits + 31) / 32;
+  const uint64_t words = (bit_hi - bit_lo + 31) / 32;
   const uint64_t blocks = (words + 255) / 256;
   const uint32_t gx = (uint32_t)std::min<uint64_t>(blocks, (uint64_t)sm_count() * 16 / n_experts + 1);
   auto kern = ((thresh << 11) & 0xffffffffull) == 0 ? k_mask_bitmap<true> : k_mask_bitmap<false>;
-  kern<<<dim3(gx, n_experts), 256, 0, (cudaStream_t)stream>>>(lo, hi, n_experts, thresh, n_bits, bitmap, words_per_row);
+  kern<<<dim3(gx, n_experts), 256, 0, (cudaStream_t)stream>>>(lo, hi, n_experts, thresh, bit_lo / 32, bit_hi, bitmap,
+                                                              words_per_row);
   return launch_status("rlk_fusion_mask_bitmap");
+}
+
+int rlk_fusion_mask_bitmap(const uint64_t* child_seeds, int n_experts, uint64_t thresh, uint64_t n_bits,
+                           uint32_t* bitmap, uint64_t words_per_row, void* stream) {
+  return rlk_fusion_mask_bitmap_range(child_seeds, n_experts, thresh, 0, n_bits, bitmap, words_per_row, stream);
 }
 
 int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, int dtype_out, int delta_mode,

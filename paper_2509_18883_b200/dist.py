@@ -6,7 +6,8 @@ items from its own start) is split into world-size contiguous ranges balanced by
 range of the output.  The one exchange is the all_reduce of the f64 norm partials between K1 and
 finalize -- every (item, expert) slot is produced by exactly one rank and is exactly zero elsewhere,
 so the NCCL sum is exact and the norms (hence scales, masks, erase decisions and outputs) are
-bit-identical at every world size.  FusionStats counters are summed by a second (int64) all_reduce
+bit-identical at every world size.  The dropout keep bitmap is drawn 1/world per rank and
+all-gathered (one collective per expert row), so no rank draws the whole embedding-sized rows.  FusionStats counters are summed by a second (int64) all_reduce
 only when statistics are requested.
 
 The GRPO loss shards by response; per-group token-term sums are all-reduced (objective.grpo_forward).
@@ -37,6 +38,24 @@ def allreduce_counts(counts: torch.Tensor, group) -> torch.Tensor:
     if group is not None:
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     return counts
+
+
+def allgather_bitmap_rows(bitmap2d: torch.Tensor, words_per_rank: int, group) -> torch.Tensor:
+    """In-place all-gather of a [N, world * words_per_rank] keep bitmap whose rank-r column slice
+    [r * words_per_rank, (r + 1) * words_per_rank) each rank has drawn (one collective per expert row)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    lo = rank * words_per_rank
+    for i in range(bitmap2d.shape[0]):
+        row = bitmap2d[i]
+        mine = row[lo:lo + words_per_rank]
+        if row.is_cuda:
+            dist.all_gather_into_tensor(row, mine, group=group)
+        else:  # gloo: list form
+            parts = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(parts, mine.clone(), group=group)
+            row.copy_(torch.cat(parts))
+    return bitmap2d
 
 
 def rank_pieces(layout: FusionLayout, world: int, rank: int) -> list[tuple[int, int, int]]:

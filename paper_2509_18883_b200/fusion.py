@@ -265,13 +265,34 @@ class FusionCall:
         counts the non-zero entries after dropout, and K3."""
         if self.dropout_mode != 2:
             return
-        n_bits = ((self.plan.max_extent + 8191) // 8192) * 8192
-        self.words_per_row = n_bits // 32
+        world, rank = 1, 0
+        if self.group is not None:
+            import torch.distributed as dist
+            world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        seeds = (L.C.c_uint64 * self.n)(*self.seeds)
+        if world == 1:
+            n_bits = ((self.plan.max_extent + 8191) // 8192) * 8192
+            self.words_per_row = n_bits // 32
+            self._alloc_bitmap()
+            self._launch("rlk_fusion_mask_bitmap", seeds, self.n, self.thresh, n_bits, L.ptr(self.bitmap),
+                         self.words_per_row, s)
+            return
+        # sharded: every rank draws 1/world of each row (the rows span the layout's largest tensor, the
+        # same on every rank) and the slices are all-gathered -- instead of the ranks holding an
+        # embedding-sized piece each drawing the whole rows
+        n_bits = ((max(self.layout.numels) + 8191) // 8192) * 8192
+        wc = ((n_bits // 32 + world - 1) // world + 3) // 4 * 4  # words per rank slice, 16-byte multiple
+        self.words_per_row = wc * world
+        self._alloc_bitmap()
+        lo, hi = min(rank * wc * 32, n_bits), min((rank + 1) * wc * 32, n_bits)
+        self._launch("rlk_fusion_mask_bitmap_range", seeds, self.n, self.thresh, lo, hi, L.ptr(self.bitmap),
+                     self.words_per_row, s)
+        from .dist import allgather_bitmap_rows
+        allgather_bitmap_rows(self.bitmap.view(self.n, self.words_per_row), wc, self.group)
+
+    def _alloc_bitmap(self) -> None:
         if self.bitmap is None or self.bitmap.numel() != self.n * self.words_per_row:
             self.bitmap = torch.empty(self.n * self.words_per_row, dtype=torch.int32, device=self.device)
-        seeds = (L.C.c_uint64 * self.n)(*self.seeds)
-        self._launch("rlk_fusion_mask_bitmap", seeds, self.n, self.thresh, n_bits, L.ptr(self.bitmap),
-                     self.words_per_row, s)
 
     # -- K1 + all_reduce + finalize
     def norms(self, precomputed_sumsq: torch.Tensor | None = None) -> "FusionCall":

@@ -18,7 +18,7 @@ def declared_symbols():
 
 def test_header_declares_hot_path():
     syms = declared_symbols()
-    for s in ["rlk_fusion_sumsq", "rlk_fusion_finalize", "rlk_fusion_mask_bitmap", "rlk_fusion_merge",
+    for s in ["rlk_fusion_sumsq", "rlk_fusion_finalize", "rlk_fusion_mask_bitmap", "rlk_fusion_mask_bitmap_range", "rlk_fusion_merge",
               "rlk_grpo_fwd", "rlk_grpo_bwd", "rlk_last_error"]:
         assert s in syms
 

@@ -64,7 +64,20 @@ def _worker(rank, world, port, q):
         allreduce_counts(c, dist.group.WORLD)
         gs = torch.tensor([0.25 * (rank + 1), -1.0], dtype=torch.float64)
         dist.all_reduce(gs)
-        q.put((rank, exact, c.tolist(), gs.tolist()))
+        # keep bitmap: each rank draws its column slice of every expert row, then the rows are gathered
+        from oracle import rng as ORNG
+        from paper_2509_18883_b200.dist import allgather_bitmap_rows
+        n_bits = 40960
+        wc = ((n_bits // 32 + world - 1) // world + 3) // 4 * 4
+        rows = [np.packbits(ORNG.keep_mask(ORNG.fusion_child_seed(42, i), 0, n_bits, 0.5), bitorder="little")
+                .view(np.int32) for i in range(3)]
+        bm = torch.full((3, wc * world), -7, dtype=torch.int32)
+        lo, hi = rank * wc, min((rank + 1) * wc, n_bits // 32)
+        for i in range(3):
+            bm[i, lo:hi] = torch.from_numpy(rows[i][lo:hi].copy())
+        allgather_bitmap_rows(bm, wc, dist.group.WORLD)
+        bm_ok = all(np.array_equal(bm[i, :n_bits // 32].numpy(), rows[i]) for i in range(3))
+        q.put((rank, exact, c.tolist(), gs.tolist(), bm_ok))
     finally:
         dist.destroy_process_group()
 
@@ -86,7 +99,8 @@ def test_gloo_world2_exact_partials_and_counts():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, exact, counts, gs in res:
+    for rank, exact, counts, gs, bm_ok in res:
         assert exact, f"rank {rank}: sharded partials differ from the world-1 table"
+        assert bm_ok, f"rank {rank}: gathered keep bitmap differs from the full rows"
         assert counts == [3, 30]
         assert gs == [0.75, -2.0]

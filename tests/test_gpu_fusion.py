@@ -182,6 +182,13 @@ def test_mask_bitmap_bit_exact(cuda):
         for i in range(3):
             ref = OR.keep_mask(OR.fusion_child_seed(42, i), 0, n_bits, p)
             assert np.array_equal(bits[i].astype(bool), ref)
+        # the sharded form: 3 'ranks' each draw one slice of every row (rlk_fusion_mask_bitmap_range)
+        part = torch.full_like(bm, -1)
+        cuts = [0, 11 * 32 * 1024, 23 * 32 * 1024, n_bits]
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            L.call("rlk_fusion_mask_bitmap_range", (L.C.c_uint64 * 3)(*seeds), 3, keep_threshold(p), lo, hi,
+                   L.ptr(part), wpr, L.stream_handle())
+        assert torch.equal(part, bm)
 
 
 def test_fast_path_equals_exact_path_random(cuda, monkeypatch):
