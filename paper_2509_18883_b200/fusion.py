@@ -449,6 +449,9 @@ def _flat(t: torch.Tensor) -> torch.Tensor:
 
 def _compute_norms(taus: Sequence[TaskVector]) -> None:
     """Fill `_norm` for every vector lacking it: one K1 launch per distinct storage mode/dtype."""
+    for t in taus:
+        if t._norm is None and t.numel == 0:
+            t._norm = 0.0  # np.linalg.norm of an empty array
     todo = [t for t in taus if t._norm is None]
     if not todo:
         return
@@ -567,6 +570,12 @@ def fuse(theta_sft: ParamTable, taus: Sequence[TaskVector], cfg: FusionConfig,
     if cfg.merge_weights is not None and len(cfg.merge_weights) != len(taus):
         raise ValueError("merge_weights length must match the expert count")
     weights = cfg.merge_weights or tuple(1.0 / len(taus) for _ in taus)
+    if theta_sft.logits.numel() == 0:
+        # an empty table: every norm is 0, so the mean target has no non-zero norm (fusion.py:97-98),
+        # and otherwise the kept fraction count_nonzero / size divides by zero (fusion.py:172-174)
+        if cfg.target_mode == 1:
+            raise ValueError("cannot take mean norm of all-zero task vectors")
+        raise ZeroDivisionError("float division by zero")
 
     base = theta_sft.logits
     pair = all(t.is_pair and t._base.data_ptr() == base.data_ptr() and t._expert.dtype == base.dtype

@@ -106,6 +106,14 @@ def test_fuse_validation_messages(cuda):
         F.fuse(b, [F.task_vector(b, b)], F.FusionConfig())
     with pytest.raises(ValueError, match="logits must be finite"):
         F.ParamTable(torch.tensor([[[1.0, float("nan")]]], device=cuda))
+    # an empty table, as the reference: no non-zero norm for the mean target; else 0 / 0 in the stats
+    z = _pt(np.zeros(0), torch.float64, cuda)
+    tz = F.task_vector(z, z)
+    assert tz.norm == 0.0
+    with pytest.raises(ValueError, match="cannot take mean norm of all-zero task vectors"):
+        F.fuse(z, [tz, tz], F.FusionConfig())
+    with pytest.raises(ZeroDivisionError):
+        F.fuse(z, [tz, tz], F.FusionConfig(target_norm=None, dropout_p=0.5))
     # identity round trip: 1 expert, w=1, p=0, erase off
     fused, _ = F.fuse(b, [F.task_vector(e, b)], F.FusionConfig(target_norm=None, erase_mode=False))
     assert torch.equal(fused.logits, e.logits)
