@@ -193,22 +193,28 @@ def fusion_bench(args, rank, world, local, group):
                total_params=layout.total, n_tensors=layout.n_tensors, clocks=clocks, nonfinite=nonfinite,
                dropout_mode=call.dropout_mode, launches_per_step=(4 if cfg.dropout_p > 0 else 3))
 
-    # p = 0 variant (the reference default config): same buffers
+    # SURVEY 8(d) variants on the same buffers: p = 0 (the reference default config), squared-vote
+    # erasure, seed 0, and no normalisation (target_norm=None; K1 still runs: FusionStats.norms_before)
     if not args.quick:
-        call0 = F.FusionCall(pieces, layout, N_EXPERTS, F.FusionConfig(), group=group, stream=stream)
-        for _ in range(2):
-            call0.run(weights)
-        barrier(group)
-        torch.cuda.synchronize(dev)
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(args.steps):
-            call0.run(weights)
-        a1.record(stream)
-        torch.cuda.synchronize(dev)
-        ms0, = max_over_ranks([a0.elapsed_time(a1) / args.steps], group)
-        res["p0_ms"] = ms0
-        del call0
+        res["variants"] = {}
+        for vname, vcfg in (("p0_default_cfg", F.FusionConfig()),
+                            ("p05_squared_erase", F.FusionConfig(dropout_p=0.5, seed=42, erase_weighting="squared")),
+                            ("p05_seed0", F.FusionConfig(dropout_p=0.5, seed=0)),
+                            ("p05_no_normalize", F.FusionConfig(dropout_p=0.5, seed=42, target_norm=None))):
+            call0 = F.FusionCall(pieces, layout, N_EXPERTS, vcfg, group=group, stream=stream)
+            for _ in range(2):
+                call0.run(weights)
+            barrier(group)
+            torch.cuda.synchronize(dev)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(args.steps):
+                call0.run(weights)
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms0, = max_over_ranks([a0.elapsed_time(a1) / args.steps], group)
+            res["variants"][vname] = ms0
+            del call0
 
     # e2e through the public API with pinned host buffers
     if not args.no_e2e:
@@ -569,8 +575,8 @@ def main():
         "clocks": fz["clocks"],
         "gpu_launches": fz["launches_per_step"] * args.steps,
     }
-    if "p0_ms" in fz:
-        line["variants"] = {"p0_default_cfg": {"value": total / (fz["p0_ms"] / 1e3), "ms_per_step": fz["p0_ms"]}}
+    if "variants" in fz:
+        line["variants"] = {k: {"value": total / (ms / 1e3), "ms_per_step": ms} for k, ms in fz["variants"].items()}
     if "e2e_ms" in fz:
         line["e2e"] = {"value": total / (fz["e2e_ms"] / 1e3), "unit": "params/s",
                        "h2d_bytes_per_step": fz["h2d"], "d2h_bytes_per_step": fz["d2h"],

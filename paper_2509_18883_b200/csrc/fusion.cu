@@ -843,7 +843,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
       const uint8_t* bm = sb + (N + 1) * SB;
       const uint32_t nvec = main_elems / kFastElems;
       const uint64_t out_base = g.start + off;
-      for (uint32_t v = fast_ok ? tid : nvec; v < nvec; v += kFastCThreads) {
+      // elements whose guard trips are only recorded here (bit 4 j + e: iteration j, element e) and
+      // recomputed after the stage's fast loop, so the hot loop carries no slow-path code and a warp
+      // pays max-over-lanes(popcount) slow rounds per stage, not one per element position per iteration
+      static_assert(ELEMS / kFastElems / kFastCThreads * kFastElems <= 32, "slow bits per stage exceed a word");
+      uint32_t slowbits = 0, jit = 0;
+      for (uint32_t v = fast_ok ? tid : nvec; v < nvec; v += kFastCThreads, jit += kFastElems) {
         const uint32_t le = v * kFastElems;
         const FastVec bw4 = FastVec::load(sb + v * (2 * kFastElems));
         FastVec xw4[N];
@@ -951,34 +956,31 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
 #pragma unroll
           for (int e = 0; e < kFastElems; ++e) slowm |= (uint32_t)(gm[e] < 0.f) << e;
         }
-        if (slowm) {  // phase 2 (rare): exact reference-order evaluation of flagged elements
-#pragma unroll
-          for (int e = 0; e < kFastElems; ++e) {
-            if ((slowm >> e) & 1u) {
-              const uint32_t bw = bw4.w[e >> 1];
-              const float be = (e & 1) ? bf16_hi(bw) : bf16_lo(bw);
-              FArr<N> xe;
-              uint32_t keep = 0;
-#pragma unroll
-              for (int i = 0; i < N; ++i) {
-                const uint32_t xw = xw4[i].w[e >> 1];
-                xe.v[i] = (e & 1) ? bf16_hi(xw) : bf16_lo(xw);
-                keep |= ((kb[i] >> e) & 1u) << i;
-              }
-              uint32_t nzm, erm;
-              const double Y = merge_elem_slow<N>(be, xe, keep, &a, scale, &nzm, &erm);
-              if constexpr (kErase) {
-                const uint32_t fo = fast_opp_bits<N>(be, xe.v, keep, sr32, ERASE, false);
-#pragma unroll
-                for (int i = 0; i < N; ++i) cnt_er[i] += ((erm >> i) & 1u) - ((fo >> i) & 1u);
-              }
-              const uint32_t hb = f64_to_bf16_rne(Y);
-              uint32_t& w = outw[e >> 1];
-              w = (e & 1) ? ((w & 0x0000ffffu) | (hb << 16)) : ((w & 0xffff0000u) | hb);
-            }
-          }
-        }
+        slowbits |= slowm << jit;
         FastVec::store(outp + out_base + le, outw);
+      }
+      // phase 2 (rare): exact reference-order evaluation of the recorded elements, read back from the
+      // stage; the 2-byte store follows this thread's own vector store of the same word
+      while (slowbits) {
+        const uint32_t bpos = __ffs(slowbits) - 1;
+        slowbits &= slowbits - 1;
+        const uint32_t le = (tid + (bpos / kFastElems) * kFastCThreads) * kFastElems + (bpos % kFastElems);
+        const float be = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(sb)[le] << 16);
+        FArr<N> xe;
+        uint32_t keep = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          xe.v[i] = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le] << 16);
+          keep |= DROP ? (((uint32_t)bm[i * BMB + (le >> 3)] >> (le & 7)) & 1u) << i : (1u << i);
+        }
+        uint32_t nzm, erm;
+        const double Y = merge_elem_slow<N>(be, xe, keep, &a, scale, &nzm, &erm);
+        if constexpr (kErase) {
+          const uint32_t fo = fast_opp_bits<N>(be, xe.v, keep, sr32, ERASE, false);
+#pragma unroll
+          for (int i = 0; i < N; ++i) cnt_er[i] += ((erm >> i) & 1u) - ((fo >> i) & 1u);
+        }
+        outp[out_base + le] = (uint16_t)f64_to_bf16_rne(Y);
       }
       // items the fast path cannot certify, and the < 16-byte tail: exact f64 path
       const uint32_t e0 = fast_ok ? main_elems : 0;
