@@ -41,8 +41,9 @@ def allreduce_counts(counts: torch.Tensor, group) -> torch.Tensor:
 
 
 def allgather_bitmap_rows(bitmap2d: torch.Tensor, words_per_rank: int, group) -> torch.Tensor:
-    """In-place all-gather of a [N, world * words_per_rank] keep bitmap whose rank-r column slice
-    [r * words_per_rank, (r + 1) * words_per_rank) each rank has drawn (one collective per expert row)."""
+    """All-gather of a [N, world * words_per_rank] keep bitmap whose rank-r column slice
+    [r * words_per_rank, (r + 1) * words_per_rank) each rank has drawn, into the same buffer (one
+    collective per expert row)."""
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     lo = rank * words_per_rank
@@ -50,7 +51,8 @@ def allgather_bitmap_rows(bitmap2d: torch.Tensor, words_per_rank: int, group) ->
         row = bitmap2d[i]
         mine = row[lo:lo + words_per_rank]
         if row.is_cuda:
-            dist.all_gather_into_tensor(row, mine, group=group)
+            # a separate send buffer (an in-place all-gather would alias the receive buffer)
+            dist.all_gather_into_tensor(row, mine.clone(), group=group)
         else:  # gloo: list form
             parts = [torch.empty_like(mine) for _ in range(world)]
             dist.all_gather(parts, mine.clone(), group=group)
