@@ -111,7 +111,10 @@ int rlk_fusion_mask_bitmap_range(const uint64_t* child_seeds, int n_experts, uin
  * dropout_mode: 0 none, 1 inline SplitMix64, 2 bitmap (bitmap/words_per_row from K2).
  * keep_prob = 1 - p (f64, as the reference computes it).  erase_mode: 0 off, 1 sum, 2 squared.
  * counters: device [n_tensors * 2N] u64, accumulated (caller zeroes): K3 adds the entries erased at
- * [t*2N + N + i] (the non-zero-after-dropout counts at [t*2N + i] come from K1). */
+ * [t*2N + N + i] (the non-zero-after-dropout counts at [t*2N + i] come from K1).
+ * bf16 -> bf16 with N <= 4 and dropout_mode 0/2 runs the f32x2 fast kernel with certified guards
+ * (bit-identical to the f64 path); environment variable RLK_MERGE_FAST=0 forces the f64 path (a test
+ * hook: the results are the same either way). */
 int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, int dtype_out,
                      int delta_mode, const double* scale, const double* weights, int dropout_mode,
                      const uint64_t* child_seeds, uint64_t thresh, double keep_prob,
