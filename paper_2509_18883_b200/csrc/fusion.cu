@@ -428,36 +428,60 @@ __global__ void k_finalize(const double* __restrict__ partials, const uint32_t* 
 // High word of mix64(z) (core.py:42-49) with the second product computed for its high word only:
 // hi32(z * K2 mod 2^64) = hi32(lo * K2lo) + lo * K2hi + hi * K2lo (mod 2^32); the final
 // z ^= z >> 31 changes the high word to h ^ (h >> 31).
-__device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
+// High word of z * kMix2 mod 2^64 after the first two SplitMix64 rounds (core.py:42-49):
+// hi32(z * K2) = hi32(lo * K2lo) + lo * K2hi + hi * K2lo (mod 2^32).
+__device__ __forceinline__ uint32_t mix64_pre_hi(uint64_t z) {
   z ^= z >> 30;
   z *= kMix1;
   z ^= z >> 27;
   const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
-  const uint32_t h = __umulhi(lo, (uint32_t)kMix2) + lo * (uint32_t)(kMix2 >> 32) + hi * (uint32_t)kMix2;
-  return h ^ (h >> 31);
+  return __umulhi(lo, (uint32_t)kMix2) + lo * (uint32_t)(kMix2 >> 32) + hi * (uint32_t)kMix2;
 }
 
-// HI: thresh << 11 has a zero low word (e.g. p = 0.5), so keep <=> high word of the draw >= its high
-// word -- exact, and the low word of the draw is never needed.
-template <bool HI>
+// bits = 2 * bits + (x >= y): one subtract-with-carry and one add-with-carry (no predicates, no SEL)
+__device__ __forceinline__ uint32_t push_ge(uint32_t bits, uint32_t x, uint32_t y) {
+  uint32_t r;
+  asm("{\n .reg .u32 t;\n sub.cc.u32 t, %1, %2;\n addc.u32 %0, %3, %3;\n}" : "=r"(r) : "r"(x), "r"(y), "r"(bits));
+  return r;
+}
+// bits = 2 * bits + (x >= y) for 64-bit x, y
+__device__ __forceinline__ uint32_t push_ge64(uint32_t bits, uint64_t x, uint64_t y) {
+  uint32_t r;
+  asm("{\n .reg .u32 t;\n sub.cc.u32 t, %1, %3;\n subc.cc.u32 t, %2, %4;\n addc.u32 %0, %5, %5;\n}"
+      : "=r"(r)
+      : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32)), "r"(bits));
+  return r;
+}
+
+// MODE 0: keep <=> mix64(c) >= t64 (full 64-bit draw).  MODE 1: t64 has a zero low word (e.g. p = 0.3
+// rounded to 2^-32 steps), so the high word decides: h ^ (h >> 31) >= t_hi.  MODE 2: additionally t_hi
+// is even (p = 0.5, 0.25, 0.75, ...): the final xor-shift only touches bit 0 of the high word, which
+// cannot move it across an even threshold, so h >= t_hi.  All three are exact.  Bits are assembled
+// from draw 31 down to draw 0 (add-with-carry doubling), so draw j lands in bit j.
+template <int MODE>
 __global__ void k_mask_bitmap(ulonglong4 seeds_lo, ulonglong4 seeds_hi, int n, uint64_t thresh, uint64_t w_lo,
                               uint64_t n_bits, uint32_t* __restrict__ bitmap, uint64_t words_per_row) {
   // keep iff (mix64(c_j) >> 11) >= thresh  <=>  mix64(c_j) >= thresh << 11  (thresh <= 2^53)
   const uint64_t t64 = thresh << 11;
   const uint32_t t_hi = (uint32_t)(t64 >> 32);
-  const bool all = thresh == 0;  // p == 0: every draw kept (t64 == 0)
   const uint64_t words = (n_bits + 31) / 32;
   const int i = blockIdx.y;  // expert (grid.y = N): no 64-bit division per word
   const uint64_t seed = i < 4 ? (&seeds_lo.x)[i] : (&seeds_hi.x)[i - 4];
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t w = w_lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += stride) {
     uint32_t bits = 0;
-    uint64_t c = seed + (w * 32 + 1) * kGamma;  // counter of draw j = 32 w (core.py:69-71)
+    uint64_t c = seed + (w * 32 + 32) * kGamma;  // counter of draw j = 32 w + 31 (core.py:69-71)
 #pragma unroll 8
-    for (int b = 0; b < 32; ++b) {
-      const bool keep = HI ? mix64_hi(c) >= t_hi : mix64(c) >= t64;
-      bits |= (uint32_t)(all || keep) << b;
-      c += kGamma;
+    for (int b = 31; b >= 0; --b) {
+      if (MODE == 2) {
+        bits = push_ge(bits, mix64_pre_hi(c), t_hi);
+      } else if (MODE == 1) {
+        const uint32_t h = mix64_pre_hi(c);
+        bits = push_ge(bits, h ^ (h >> 31), t_hi);
+      } else {
+        bits = push_ge64(bits, mix64(c), t64);
+      }
+      c -= kGamma;
     }
     bitmap[(uint64_t)i * words_per_row + w] = bits;
   }
@@ -1210,7 +1234,9 @@ int rlk_fusion_mask_bitmap_range(const uint64_t* child_seeds, int n_experts, uin
   const uint64_t words = (bit_hi - bit_lo + 31) / 32;
   const uint64_t blocks = (words + 255) / 256;
   const uint32_t gx = (uint32_t)std::min<uint64_t>(blocks, (uint64_t)sm_count() * 16 / n_experts + 1);
-  auto kern = ((thresh << 11) & 0xffffffffull) == 0 ? k_mask_bitmap<true> : k_mask_bitmap<false>;
+  const uint64_t t64 = thresh << 11;  // thresh == 0 (p = 0): t64 == 0 keeps every draw in any mode
+  auto kern = (t64 & 0xffffffffull) != 0 ? k_mask_bitmap<0>
+              : ((t64 >> 32) & 1u) ? k_mask_bitmap<1> : k_mask_bitmap<2>;
   kern<<<dim3(gx, n_experts), 256, 0, (cudaStream_t)stream>>>(lo, hi, n_experts, thresh, bit_lo / 32, bit_hi, bitmap,
                                                               words_per_row);
   return launch_status("rlk_fusion_mask_bitmap");

@@ -179,7 +179,9 @@ def test_mask_bitmap_bit_exact(cuda):
     """K2 keep bits == the reference's `uniform >= p` draws, incl. a far index window."""
     from paper_2509_18883_b200 import _lib as L
     from paper_2509_18883_b200.core import fusion_child_seeds, keep_threshold
-    for p in (0.3, 0.5, 0.9):
+    # 0.3 / 0.9: full 64-bit compare; 1288490189 / 2^32: high-word compare with an odd threshold;
+    # 0.5 / 0.75: even high-word threshold (K2's three modes)
+    for p in (0.3, 0.5, 0.9, 1288490189 / 2**32, 0.75):
         seeds = fusion_child_seeds(42, 3)
         n_bits = 1 << 20
         wpr = n_bits // 32
