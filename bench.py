@@ -278,7 +278,7 @@ def fusion_e2e(args, pieces, call, weights, stream, dev, group):
         if api:
             with torch.cuda.stream(stream):
                 fuse_streaming(names, numels, N_EXPERTS, ArraySource(api_b, api_e), ArraySink(api_o), call.cfg,
-                               dtype=dt, device_budget_bytes=16 << 30, group_bytes=2 << 30)
+                               dtype=dt, device_budget_bytes=int(args.e2e_budget_gb * (1 << 30)), group_bytes=2 << 30)
             return
         if not pipelined:
             with torch.cuda.stream(stream):
@@ -499,6 +499,7 @@ def main():
     ap.add_argument("--layout", default="llama8b")
     ap.add_argument("--dropout", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-budget-gb", type=float, default=40.0, help="device ring for the streamed e2e step")
     ap.add_argument("--grpo-tokens", type=int, default=32768)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-grpo", action="store_true")
