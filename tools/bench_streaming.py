@@ -24,10 +24,13 @@ from paper_2509_18883_b200.loader import ArraySource, ChecksumSink, HostLoader, 
 class ReplaySource:
     """Pageable host memory (like a checkpoint in the page cache): slices of one 4 GiB random pool."""
 
-    def __init__(self, n_streams=4, pool_elems=1 << 31):
+    def __init__(self, n_streams=4, pool_elems=1 << 31, pinned=False):
         g = np.random.default_rng(0)
         self.pool = (g.standard_normal(pool_elems // 8, dtype=np.float32) * 0.02).astype(np.float32)
         self.pool = np.tile(self.pool.view(np.uint32) >> 16, 8).astype(np.uint16)
+        if pinned:  # page-locked: the loader DMAs straight from it
+            self._pinned = torch.from_numpy(self.pool.view(np.int16)).pin_memory()
+            self.pool = self._pinned.numpy().view(np.uint16)
         self.n = pool_elems
 
     def fill(self, loader, name, si, dst, stream):
@@ -38,9 +41,10 @@ class ReplaySource:
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--layers", type=int, default=1)
-ap.add_argument("--source", choices=["synth", "replay"], default="replay")
+ap.add_argument("--source", choices=["synth", "replay", "pinned"], default="replay")
 ap.add_argument("--budget-gb", type=float, default=48)
 ap.add_argument("--threads", type=int, default=0)
+ap.add_argument("--group-gb", type=float, default=2.0)
 ap.add_argument("--json-out", default=None)
 a = ap.parse_args()
 shapes = longcat_560b(n_layers=a.layers)
@@ -48,20 +52,20 @@ names = list(shapes)
 numels = [numel(s) for s in shapes.values()]
 total = sum(numels)
 full = sum(numel(s) for s in longcat_560b().values())
-src = SyntheticSource() if a.source == "synth" else ReplaySource()
+src = SyntheticSource() if a.source == "synth" else ReplaySource(pinned=a.source == "pinned")
 sink = ChecksumSink()
 ld = HostLoader(slot_bytes=64 << 20, n_slots=6, n_threads=a.threads)
 cfg = F.FusionConfig(dropout_p=0.5, seed=42)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 rep = fuse_streaming(names, numels, 3, src, sink, cfg, device_budget_bytes=int(a.budget_gb * (1 << 30)), stats=False,
-                     loader=ld)
+                     loader=ld, group_bytes=int(a.group_gb * (1 << 30)))
 dt = time.perf_counter() - t0
 ld.close()
 res = {"workload": f"config4 slice: longcat560b layout, {a.layers} layer(s) + embeddings/head, 3 experts + base, "
                    f"bf16, FusionConfig(dropout_p=0.5, seed=42), source={a.source}",
        "params": total, "full_model_params": full, "seconds": dt, "params_per_s": total / dt,
-       "h2d_gbs": rep.h2d_bytes / dt / 1e9, "d2h_gbs": rep.d2h_bytes / dt / 1e9, "groups": rep.groups,
+       "h2d_gbs": rep.h2d_bytes / dt / 1e9, "d2h_gbs": rep.d2h_bytes / dt / 1e9, "groups": rep.groups, "group_gb": a.group_gb,
        "projected_full_model_8gpu_s": full / 8 / (total / dt)}
 print(json.dumps(res))
 if a.json_out:
