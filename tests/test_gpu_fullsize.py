@@ -92,3 +92,49 @@ def test_fullsize_embedding_norms(config3):
         ref = float(np.sqrt(np.dot(d, d)))
         got = float(np.sqrt(call.sumsq[t, i].item()))
         assert got == pytest.approx(ref, rel=1e-13)
+
+
+def test_fullsize_grpo_config5_chunk(cuda):
+    """Config 5 at its launch size (2 responses x 32,768 tokens, V = 131,072 bf16 = 16 GiB of logits,
+    off-policy, tau = 0.7): the fused loss+gradient kernel agrees with the K4 forward on J and every
+    row's coefficient; sampled rows (incl. the first and last) match the oracle's logp / term / coef
+    and gradient rows; every gradient row sums to ~0 (softmax sums to one)."""
+    from paper_2509_18883_b200 import _lib as L
+    from paper_2509_18883_b200 import objective as O
+    from oracle import objective as OO
+    torch.cuda.empty_cache()
+    if torch.cuda.mem_get_info()[0] < 40 << 30:
+        pytest.skip("needs ~40 GB of free HBM")
+    V, T = 131072, 32768
+    R = 2 * T
+    lg = torch.empty((R, V), dtype=torch.bfloat16, device=cuda)
+    L.call("rlk_synth_normal", L.ptr(lg), L.RLK_BF16, lg.numel(), 0, 99, 2.0, None, L.stream_handle())
+    g = np.random.default_rng(5)
+    toks = g.integers(0, V, R)
+    lt = g.normal(-12.0, 0.3, R)
+    li = lt + g.normal(0, 0.05, R)
+    adv = np.array([1.0, -1.0])
+    b = O.GRPOBatch.pack(toks, lt, li, [0, T, R], adv, [1, 1], 2, T, temperature=0.7, device=cuda)
+    fwd = O.grpo_forward(lg, b)
+    fused, grad = O.grpo_forward_backward(lg, b)
+    assert float(fused.objective) == pytest.approx(float(fwd.objective), rel=1e-5)
+    np.testing.assert_allclose(fused.coef.cpu().numpy(), fwd.coef.cpu().numpy(), rtol=1e-4, atol=1e-14)
+    rows = np.unique(np.concatenate([[0, T - 1, T, R - 1], g.integers(0, R, 28)]))
+    z = lg[torch.from_numpy(rows).to(cuda)].float().double().cpu().numpy()
+    clip = dict(eps_neg_low=0.2, eps_pos_high=0.2, eps_neg_high=3.0, tis_cap=2.0, guard_positive=True)
+    sample = (rows >= T).astype(np.int64)
+    logp, term, coef = OO.token_terms(z, None, toks[rows], lt[rows], li[rows], sample, adv, [1, 1], [0.7, 0.7],
+                                      clip, norm=1.0 / (1 * 2 * T))
+    # K4 sums 2^x in f32 per thread over the 131,072-wide row (f64 combine): logp to ~1e-7 absolute
+    np.testing.assert_allclose(fwd.logp.cpu().numpy()[rows], logp, rtol=0, atol=2e-6)
+    np.testing.assert_allclose(fwd.term.cpu().numpy()[rows], term, rtol=1e-5, atol=1e-15)
+    np.testing.assert_allclose(fwd.coef.cpu().numpy()[rows], coef, rtol=1e-5, atol=1e-18)
+    gref = OO.gradient_rows(z, None, toks[rows], coef, [0.7] * len(rows), z.shape)
+    gg = grad[torch.from_numpy(rows).to(cuda)].float().double().cpu().numpy()
+    scale = np.abs(coef).max()
+    np.testing.assert_allclose(gg, gref, rtol=0, atol=1e-2 * scale + 1e-15)
+    sums = grad.float().sum(dim=1).double().cpu().numpy()
+    cmax = np.abs(fused.coef.cpu().numpy())
+    assert np.all(np.abs(sums) <= 1e-2 * cmax + 1e-12)
+    del lg, grad
+    torch.cuda.empty_cache()
