@@ -104,6 +104,8 @@ class SyntheticSource:
 class ArraySink:
     def __init__(self, out: Mapping):
         self.out = out
+        # page-locked outputs are written by direct async DMA; anything else is staged synchronously
+        self.blocking = not all(isinstance(v, torch.Tensor) and v.is_pinned() for v in out.values())
 
     def drain(self, loader: HostLoader, name: str, src: torch.Tensor, stream) -> None:
         dst = self.out[name]
@@ -114,6 +116,8 @@ class ArraySink:
 
 class ChecksumSink:
     """Keeps a 64-bit checksum per tensor instead of the fused values (for outputs larger than RAM)."""
+
+    blocking = True  # host pass over every chunk
 
     def __init__(self):
         self.sums: dict[str, int] = {}
@@ -167,7 +171,9 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
     `device_budget_bytes`.  Three streams: H2D of group g + 1, the fusion kernels of group g and the
     D2H of group g - 1 run concurrently (PCIe is full duplex); a group's H2D waits (on events, not on
     the host) for the D2H of every earlier group whose ring space it reuses.  Pinned host
-    sources/sinks are DMA'd directly; pageable ones go through the loader's pinned slots."""
+    sources/sinks are DMA'd directly; pageable ones go through the loader's pinned slots.  Blocking
+    sinks (pageable outputs, checksums) run on a worker thread with their own loader, overlapping the
+    main thread's H2D staging."""
     dev = torch.device("cuda", torch.cuda.current_device())
     esize = torch.tensor([], dtype=dtype).element_size()
     cap = device_budget_bytes // esize // 64 * 64  # ring capacity in elements
@@ -212,15 +218,36 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
     # every launch plan is built before the first bulk copy: its small blocking uploads must not queue
     # behind gigabytes of H2D traffic (and pinned staging for them would not recycle in time)
     plans = [build(gi, group) for gi, group in enumerate(groups)]
-    freed: dict[int, torch.cuda.Event] = {}  # group -> its D2H has completed
+    # Sinks run on a worker thread with a loader of their own: a pageable sink's staged D2H (and a
+    # checksum sink's host pass) then overlaps the main thread's staging of the next groups' H2D,
+    # instead of leaving PCIe idle in between (ctypes releases the GIL inside the C calls).
+    # Sinks that block the host (pageable outputs, checksums) do not need the host thread that stages
+    # H2D: with a non-blocking sink (page-locked outputs, direct DMA) everything stays on this thread.
+    import concurrent.futures as cf
+    blocking = getattr(sink, "blocking", True)
+    drain_pool = cf.ThreadPoolExecutor(max_workers=1) if blocking else None
+    drain_loader = HostLoader() if blocking else loader
+    freed: dict[int, cf.Future] = {}  # group -> future of the event marking its D2H complete
     pending = None  # (group index, out views, compute-done event)
+
+    def drain_on_worker(pend):
+        with torch.cuda.device(dev):  # the worker thread's current device is not inherited
+            return _drain(pend, drain_loader, sink, d2h_s, names, rep, groups)
+
+    def drain_async(pend):
+        if drain_pool is None:
+            f = cf.Future()
+            f.set_result(_drain(pend, loader, sink, d2h_s, names, rep, groups))
+            return f
+        return drain_pool.submit(drain_on_worker, pend)
+
     try:
         for gi, (group, views_all, call) in enumerate(plans):
             for j in waits[gi]:
                 if pending is not None and pending[0] == j:  # ring too small to overlap: drain now
-                    freed[j] = _drain(pending, loader, sink, d2h_s, names, rep, groups)
+                    freed[j] = drain_async(pending)
                     pending = None
-                h2d_s.wait_event(freed.pop(j))
+                h2d_s.wait_event(freed.pop(j).result())
             for t, views in zip(group, views_all):
                 for si in range(n_experts + 1):
                     source.fill(loader, names[t], si, views[si], h2d_s)
@@ -233,10 +260,12 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
             done.record(comp_s)
             # drain the previous group while this one computes
             if pending is not None:
-                freed[pending[0]] = _drain(pending, loader, sink, d2h_s, names, rep, groups)
+                freed[pending[0]] = drain_async(pending)
             pending = (gi, [v[-1] for v in views_all], done)
         if pending is not None:
-            _drain(pending, loader, sink, d2h_s, names, rep, groups)
+            freed[pending[0]] = drain_async(pending)
+        for f in freed.values():
+            f.result()  # re-raises a sink error
         torch.cuda.synchronize(dev)
         if stats:
             for group, _, call in plans:
@@ -244,6 +273,9 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
                 for k, t in enumerate(group):
                     rep.stats[names[t]] = call.stats(k, weights, host=host)
     finally:
+        if drain_pool is not None:
+            drain_pool.shutdown(wait=True)
+            drain_loader.close()
         if own_loader:
             loader.close()
     return rep
