@@ -138,6 +138,10 @@ def barrier(group):
 
 
 # ----------------------------------------------------------------------------------- fusion
+def local_params_of(pieces) -> int:
+    return sum(p.numel for p in pieces)
+
+
 def fusion_bench(args, rank, world, local, group):
     import torch
     from paper_2509_18883_b200 import fusion as F
@@ -147,7 +151,7 @@ def fusion_bench(args, rank, world, local, group):
     numels = [numel(s) for s in shapes.values()]
     layout = F.FusionLayout(numels)
     dev = torch.device("cuda", local)
-    dt = torch.bfloat16
+    dt = {"bf16": torch.bfloat16, "f32": torch.float32}[args.dtype]
     stream = torch.cuda.Stream(dev)
     pieces = []
     with torch.cuda.stream(stream):
@@ -163,18 +167,36 @@ def fusion_bench(args, rank, world, local, group):
     weights = tuple(1.0 / N_EXPERTS for _ in range(N_EXPERTS))
     call = F.FusionCall(pieces, layout, N_EXPERTS, cfg, group=group, stream=stream)
 
+    # inputs smaller than ~2x L2 (config 1): flush L2 between timed steps (a 512 MiB write, outside
+    # the per-step events); larger inputs stream through L2 on their own
+    in_bytes = local_params_of(pieces) * dt.itemsize * (N_EXPERTS + 1)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if in_bytes < (256 << 20) else None
+
     def timed(steps, profile):
         call.timers = {} if profile else None
         barrier(group)
         torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        if flush is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                call.run(weights)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier(group)
+            return e0.elapsed_time(e1) / steps
+        evs = []
         for _ in range(steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             call.run(weights)
-        e1.record(stream)
+            e1.record(stream)
+            evs.append((e0, e1))
         torch.cuda.synchronize(dev)
         barrier(group)
-        return e0.elapsed_time(e1) / steps
+        return sum(a.elapsed_time(b) for a, b in evs) / steps
 
     for _ in range(args.warmup):
         call.run(weights)
@@ -190,6 +212,9 @@ def fusion_bench(args, rank, world, local, group):
     st = call.check_status(per_tensor_raise=False)
     nonfinite = int((st == 2).sum())
     res = dict(ms=ms_max, ms_local=ms, kern_local=kern, kern_max=kmax, local_params=local_params,
+               l2=("L2 flushed (512 MiB write) before every timed step; inputs "
+                   f"{in_bytes / 2**20:.0f} MiB" if flush is not None else
+                   f"inputs {in_bytes / 1e9:.0f} GB >> 126 MB L2; no flush needed"),
                total_params=layout.total, n_tensors=layout.n_tensors, clocks=clocks, nonfinite=nonfinite,
                dropout_mode=call.dropout_mode, launches_per_step=(4 if cfg.dropout_p > 0 else 3))
 
@@ -497,6 +522,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--layout", default="llama8b")
+    ap.add_argument("--dtype", choices=["bf16", "f32"], default="bf16", help="parameter dtype (config 1 is f32)")
     ap.add_argument("--dropout", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-budget-gb", type=float, default=40.0, help="device ring for the streamed e2e step")
@@ -510,7 +536,9 @@ def main():
     args.warmup = max(args.warmup, 3)
     rank, world, local, group = dist_setup(args)
     peak, peak_src = measured_peak_gbs()
-    workload = (f"config3: {N_EXPERTS} experts + base, Llama-3-8B-shaped bf16 state dict ({args.layout}), "
+    cname = {"mlp10m": "config1: toy-MLP-shaped", "gpt1p3b": "config2: GPT-1.3B-shaped",
+             "llama8b": "config3: Llama-3-8B-shaped", "longcat560b": "config4: LongCat-560B-shaped"}[args.layout]
+    workload = (f"{cname} {args.dtype} state dict ({args.layout}), {N_EXPERTS} experts + base, "
                 f"FusionConfig(dropout_p={args.dropout}, seed=42, erase sum, mean-norm), sharded by param range")
 
     if args.impl == "reference":
@@ -548,7 +576,8 @@ def main():
     ms = fz["ms"]
     value = total / (ms / 1e3)
     # dominant kernel roofline (rank 0's launches; algorithmic bytes = SURVEY 8(d) per-param figures)
-    kb = {"rlk_fusion_sumsq": (N_EXPERTS + 1) * 2, "rlk_fusion_merge": (N_EXPERTS + 1) * 2 + 2}
+    es = {"bf16": 2, "f32": 4}[args.dtype]
+    kb = {"rlk_fusion_sumsq": (N_EXPERTS + 1) * es, "rlk_fusion_merge": (N_EXPERTS + 1) * es + es}
     kern = {k: v for k, v in fz["kern_local"].items() if k in kb}
     dom = max(kern, key=kern.get)
     achieved = fz["local_params"] * kb[dom] / (kern[dom] / 1e3) / 1e9
@@ -560,14 +589,14 @@ def main():
             traffic = tj.get(args.layout, {}).get(f"{world}", {}).get(dom)
         except Exception:
             traffic = None
-    step_gbs = (total * 2 * (N_EXPERTS + 1) * 2 + total * 2) / (ms / 1e3) / 1e9
+    step_gbs = (total * es * (N_EXPERTS + 1) * 2 + total * es) / (ms / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (counter-hash normal, SURVEY 8(d))",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-hash normal, SURVEY 8(d))",
         "config": {"workload": workload, "params": total, "tensors": fz["n_tensors"], "experts": N_EXPERTS,
                    "parallelism": f"param-range shards x{world}, NCCL all_reduce of norm partials",
-                   "l2": "inputs 80 GB >> 126 MB L2; no flush needed",
+                   "l2": fz["l2"],
                    "dropout_mode": {1: "inline", 2: "bitmap"}.get(fz["dropout_mode"], "none")},
         "hbm_gbs_step": step_gbs, "hbm_frac_step": step_gbs / peak,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

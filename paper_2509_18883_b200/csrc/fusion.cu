@@ -626,7 +626,7 @@ __device__ __forceinline__ uint32_t word_of(const uint4& q, int p) {
 
 // Generic K3: the reference-order f64 path for every dtype combination (and the tails).
 template <int DTI, int DTO, int N>
-__global__ void __launch_bounds__(kThreads, 1) k_merge(const __grid_constant__ MergeArgs a) {
+__global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid_constant__ MergeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DTI>::size;
   constexpr int VEC = 16 / ESZ;
@@ -1117,11 +1117,15 @@ static int launch_merge(MergeArgs& a, cudaStream_t s) {
   if constexpr (DTI == RLK_BF16 && DTO == RLK_BF16 && N <= 4) {
     if (a.fast && !a.delta_mode && a.with_base && a.dropout_mode != 1) return dispatch_fast<N>(a, s);
   }
+  // two CTAs per SM (N <= 5; more experts would spill): the reference-order f64 arithmetic is
+  // latency-bound, so it needs the warps
+  constexpr uint32_t ctas = N <= 5 ? 2u : 1u;
+  if (ctas == 2) a.nstages = ns = std::max<uint32_t>(2u, std::min<uint32_t>(ns / 2, 4u));
   const uint32_t smem = 1024 + sb * ns;
   auto kern = k_merge<DTI, DTO, N>;
   int st = ensure_smem(kern, smem);
   if (st) return st;
-  uint32_t grid = std::min<uint32_t>(a.plan.n_items, (uint32_t)sm_count());
+  uint32_t grid = std::min<uint32_t>(a.plan.n_items, ctas * (uint32_t)sm_count());
   kern<<<grid, kThreads, smem, s>>>(a);
   return launch_status("rlk_fusion_merge");
 }

@@ -18,8 +18,11 @@ tag = sys.argv[1]
 src = ROOT / "gpurun_out" / tag
 dst = ROOT / "profiles"
 
-# 1. bench line
+# 1. bench lines (config 3 headline; configs 1, 2 and the config-4 streaming slices when present)
 shutil.copy(src / "bench.json", dst / f"{tag}_bench.json")
+for extra in ("bench_config2.json", "bench_config1.json", "config4_replay.json", "config4_pinned.json"):
+    if (src / extra).exists():
+        shutil.copy(src / extra, dst / f"{tag}_{extra}")
 
 # 2. launch list -> per-kernel averages and the fusion-step shares
 rows = list(csv.reader(open(src / "launches.csv")))
