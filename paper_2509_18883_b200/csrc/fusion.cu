@@ -789,6 +789,10 @@ constexpr int kFastPairs = RLK_FAST_PAIRS;
 #endif
 constexpr uint32_t kFastSB = RLK_FAST_SB;  // bytes per stream per stage in the fast merge
 constexpr int kFastElems = 2 * kFastPairs;
+#ifndef RLK_FAST_CTAS
+#define RLK_FAST_CTAS 1
+#endif
+constexpr int kFastCtas = RLK_FAST_CTAS;  // CTAs per SM of the fast merge (the smem budget is split)
 struct FastVec {
   uint32_t w[kFastPairs];
   __device__ static FastVec load(const void* p) {
@@ -817,7 +821,7 @@ struct FastVec {
 };
 
 template <int N, int DROP, int ERASE, bool UNI>
-__global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_constant__ MergeArgs a) {
+__global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __grid_constant__ MergeArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t SB = kFastSB;
   constexpr uint32_t ELEMS = SB / 2;
@@ -885,11 +889,14 @@ __global__ void __launch_bounds__(kFastThreads, 1) k_merge_fast(const __grid_con
         // dropout on the integer side: the thread's 4 keep bits go to byte sign bits (one IMAD), PRMT
         // sign-replication turns them into halfword masks, and one LOP3 per word swaps every dropped
         // expert half for the base half, so d = x - b is exactly +0 there (reference: k = 0, fusion.py:114)
-        static_assert(kFastPairs == 2, "the keep-bit spread assumes 4 elements per thread-vector");
+        static_assert(kFastPairs == 1 || kFastPairs == 2, "the keep-bit spread handles 2 or 4 elements per thread");
+        constexpr uint32_t kSpreadMask = (1u << kFastElems) - 1u;
+        constexpr uint32_t kSpreadMul = kFastPairs == 2 ? 0x10204080u : 0x4080u;
+        constexpr uint32_t kSpreadSign = kFastPairs == 2 ? 0x80808080u : 0x8080u;
   static_assert(N <= 8, "output guard certified for N <= 11");
         uint32_t spread[N];
 #pragma unroll
-        for (int i = 0; i < N; ++i) spread[i] = DROP ? (((kb[i] & 0xfu) * 0x10204080u) & 0x80808080u) : 0u;
+        for (int i = 0; i < N; ++i) spread[i] = DROP ? (((kb[i] & kSpreadMask) * kSpreadMul) & kSpreadSign) : 0u;
         uint32_t outw[kFastPairs];
         float gm[kFastElems];  // signed guard margin per element: < 0 -> recompute exactly
 #pragma unroll
@@ -1083,12 +1090,12 @@ static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
   uint32_t sb = (N + 1) * kFastSB + (DROP ? N * (kFastSB / 2 / 8) : 0);
   sb = (sb + 127) & ~127u;
   a.stage_bytes = sb;
-  a.nstages = std::min<uint32_t>(8, (kSmemBudget - 1024) / sb);
+  a.nstages = std::min<uint32_t>(8, (kSmemBudget / kFastCtas - 1024) / sb);
   const uint32_t smem = 1024 + a.stage_bytes * a.nstages;
   auto kern = k_merge_fast<N, DROP, ERASE, UNI>;
   int st = ensure_smem(kern, smem);
   if (st) return st;
-  uint32_t grid = std::min<uint32_t>(a.plan.n_items, (uint32_t)sm_count());
+  uint32_t grid = std::min<uint32_t>(a.plan.n_items, kFastCtas * (uint32_t)sm_count());
   kern<<<grid, kFastThreads, smem, s>>>(a);
   return launch_status("rlk_fusion_merge");
 }
