@@ -43,3 +43,27 @@ def test_invalid_arguments_map_to_value_error():
         L.call("rlk_fusion_sumsq", ctypes.byref(L.FusionPlanC(0, 0, 0, 1)), 9, 0, 0, 8, None, 0, None, 0, None, 0, None)
     with pytest.raises(ValueError, match="bad dtype"):
         L.call("rlk_nonfinite_count", 8, 7, 1, 8, None)
+
+
+def test_more_argument_checks_before_any_device_work():
+    """Validation happens on the host before any CUDA call, with the reference-style message."""
+    from paper_2509_18883_b200 import _lib as L
+    L.lib()
+    seeds = (ctypes.c_uint64 * 3)(1, 2, 3)
+    with pytest.raises(ValueError, match="bad bit range"):
+        L.call("rlk_fusion_mask_bitmap_range", seeds, 3, 0, 33, 64, 8, 4, None)
+    with pytest.raises(ValueError, match="row too short"):
+        L.call("rlk_fusion_mask_bitmap_range", seeds, 3, 0, 0, 1 << 20, 8, 4, None)
+    plan = ctypes.byref(L.FusionPlanC(8, 8, 1, 1))
+    w = (ctypes.c_double * 3)(1 / 3, 1 / 3, 1 / 3)
+    with pytest.raises(ValueError, match="bad erase mode"):
+        L.call("rlk_fusion_merge", plan, 3, 0, 0, 0, 8, w, 0, None, 0, 1.0, None, 0, 5, 8, None)
+    with pytest.raises(ValueError, match="bad dropout mode"):
+        L.call("rlk_fusion_merge", plan, 3, 0, 0, 0, 8, w, 7, seeds, 0, 1.0, None, 0, 1, 8, None)
+    clip = L.ClipC(0.2, 0.2, 3.0, 2.0, 1)
+    with pytest.raises(ValueError, match="bad dtype"):
+        L.call("rlk_grpo_fwd", 8, 9, 4, 16, 16, None, 8, 8, 8, 8, 8, 8, 8, 8, ctypes.byref(clip), None, None, 8, 8, 8,
+               None, 0, None)
+    with pytest.raises(ValueError, match="multiple of 16"):
+        L.call("rlk_grpo_fused_bf16", 16, 4, 100, 100, None, 16, 8, 8, 8, 8, 8, 8, 8, ctypes.byref(clip), 1.0, None,
+               None, 8, 8, 8, 16, 100, None)
