@@ -514,6 +514,38 @@ def cpu_baseline(layout_name: str, p: float, cores: int | None = None, slice_ele
                       f"value = per-core rate (sum params / sum compute seconds) x cores"}
 
 
+def _cpu_grpo_job(args):
+    """Oracle token terms (numpy f64 log-softmax over V per token, objective.py:243-248) for a few rows."""
+    import numpy as np
+    from oracle import objective as OO
+    seed, rows, V = args
+    g = np.random.default_rng(seed)
+    z = g.normal(0, 2.0, (rows, V)).astype(np.float32).astype(np.float64)
+    toks = g.integers(0, V, rows)
+    lt = g.normal(-12, 0.3, rows)
+    clip = dict(eps_neg_low=0.2, eps_pos_high=0.2, eps_neg_high=3.0, tis_cap=2.0, guard_positive=True)
+    t0 = time.perf_counter()
+    OO.token_terms(z, None, toks, lt, lt + 0.01, np.zeros(rows, np.int64), [1.0], [1], [1.0], clip)
+    return time.perf_counter() - t0, rows
+
+
+def grpo_cpu_baseline(V: int = 131072, rows_per_job: int = 64, cores: int | None = None) -> dict:
+    """Config-5 GRPO loss on the host: the oracle's per-token log-softmax + triplet/TIS terms, one
+    process per core on a bounded sample of rows."""
+    import concurrent.futures as cf
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    cores = cores or os.cpu_count() or 1
+    jobs = [(k, rows_per_job, V) for k in range(cores)]
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        res = list(ex.map(_cpu_grpo_job, jobs))
+    cpu_s = sum(r[0] for r in res)
+    toks = sum(r[1] for r in res)
+    per_core = toks / cpu_s
+    return {"value": per_core * cores, "unit": "tokens/s", "cores": cores, "kind": "port", "per_core": per_core,
+            "sample": f"oracle token terms (numpy f64, V={V}) on {toks} synthetic rows, {rows_per_job} per process, "
+                      "one process per core; value = per-core rate x cores"}
+
+
 # ----------------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -557,15 +589,21 @@ def main():
                 "data": "synthetic", "config": {"workload": workload, "sample": vals[0]["sample"]},
                 "cpu_baseline": {k: vals[0][k] for k in ("unit", "cores", "kind", "sample")} | {"value": v},
                 "e2e": {"value": v, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        if not args.no_grpo:
+            gc = grpo_cpu_baseline()
+            line["grpo"] = {"workload": "config5 token terms, V=131072", "tokens_per_s": gc["value"],
+                            "cpu_baseline": gc}
         print(json.dumps(line))
         return
 
     import torch
     fz = fusion_bench(args, rank, world, local, group)
     gr = None if args.no_grpo else grpo_bench(args, rank, world, local, group)
-    cpu = None
+    cpu = gcpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.layout, args.dropout)
+        if gr is not None:
+            gcpu = grpo_cpu_baseline()
     if rank != 0:
         if group is not None:
             import torch.distributed as dist
@@ -629,6 +667,8 @@ def main():
                         "kernels_ms": gr["kern"]}
         if "variants" in gr:
             line["grpo"]["variants"] = gr["variants"]
+        if gcpu is not None:
+            line["grpo"]["cpu_baseline"] = gcpu
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line))
