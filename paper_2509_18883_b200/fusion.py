@@ -225,7 +225,7 @@ class FusionCall:
         self.counters = torch.zeros((nt, 2 * n_experts), dtype=torch.int64, device=self.device)
         self.partials = None
         p = cfg.dropout_p
-        if dropout_mode is None:
+        if dropout_mode is None:  # RLK_DROPOUT_MODE=1/2: test hook forcing inline / bitmap keep bits
             dropout_mode = int(os.environ.get("RLK_DROPOUT_MODE", "-1"))
         if p == 0.0:
             dropout_mode = 0
