@@ -498,7 +498,6 @@ struct MergeArgs {
   uint64_t words_per_row;
   unsigned long long* counters;
   int dropout_mode, erase_mode, delta_mode, with_base, fast;
-  uint32_t two;  // == 2 (runtime constant for the IMAD.HI counter)
   uint32_t stage_bytes, nstages;
   const uint32_t* bitmap;
 };
@@ -734,12 +733,10 @@ __device__ __forceinline__ uint32_t mask_lt0(float x) {  // 0xffffffff iff x < 0
   return r;
 }
 __device__ __forceinline__ float andnot_f(float x, uint32_t m) { return __uint_as_float(__float_as_uint(x) & ~m); }
-// c + (x >> 31) as one IMAD.HI on the FMA pipe: hi32(x * two) + c.  `two` is a runtime value (2) so
-// ptxas cannot turn it into an ALU-pipe LEA.HI.
-__device__ __forceinline__ uint32_t add_sign_bit(uint32_t x, uint32_t c, uint32_t two) {
+// c + (x >> 31): hi32(x * 2) + c (mad.hi; ptxas emits it as one LEA.HI)
+__device__ __forceinline__ uint32_t add_sign_bit(uint32_t x, uint32_t c) {
   uint32_t r;
   asm("mad.hi.u32 %0, %1, 2, %2;" : "=r"(r) : "r"(x), "r"(c));
-  (void)two;
   return r;
 }
 // PRMT in sign-replicate mode: each result byte = 0x00 / 0xFF from the sign bit of the selected byte
@@ -946,8 +943,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 #pragma unroll
               for (int i = 0; i < N; ++i) {
                 const float2 t2 = __ffma2_rn(k2[i], sg, make_float2(0.f, 0.f));
-                cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i], a.two);
-                cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i], a.two);
+                cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i]);
+                cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i]);
               }
               y2 = __ffma2_rn(make_float2(wh32[0], wh32[0]), __ffma2_rn(sg, aa, vplain), b2);
             } else {
@@ -955,8 +952,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 #pragma unroll
               for (int i = 0; i < N; ++i) {
                 const float2 t2 = __ffma2_rn(k2[i], sg, make_float2(0.f, 0.f));
-                cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i], a.two);
-                cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i], a.two);
+                cnt_er[i] = add_sign_bit(__float_as_uint(t2.x), cnt_er[i]);
+                cnt_er[i] = add_sign_bit(__float_as_uint(t2.y), cnt_er[i]);
                 const float2 tp = __fadd2_rn(t2, make_float2(fabsf(t2.x), fabsf(t2.y)));
                 acc = __ffma2_rn(make_float2(wh32[i], wh32[i]), tp, acc);
               }
@@ -1289,7 +1286,6 @@ int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, i
   a.erase_mode = erase_mode;
   a.delta_mode = delta_mode & 1;
   a.with_base = (delta_mode & 1) ? ((delta_mode >> 1) & 1) : 1;
-  a.two = 2;
   const char* env = getenv("RLK_MERGE_FAST");
   a.fast = env ? atoi(env) : 1;
   cudaStream_t s = (cudaStream_t)stream;
