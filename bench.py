@@ -172,6 +172,15 @@ def fusion_bench(args, rank, world, local, group):
     in_bytes = local_params_of(pieces) * dt.itemsize * (N_EXPERTS + 1)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if in_bytes < (256 << 20) else None
 
+    graph = None
+
+    def step(profile):
+        if graph is not None and not profile:
+            with torch.cuda.stream(stream):
+                graph.replay()
+        else:
+            call.run(weights)
+
     def timed(steps, profile):
         call.timers = {} if profile else None
         barrier(group)
@@ -180,7 +189,7 @@ def fusion_bench(args, rank, world, local, group):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(steps):
-                call.run(weights)
+                step(profile)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             barrier(group)
@@ -191,7 +200,7 @@ def fusion_bench(args, rank, world, local, group):
                 flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            call.run(weights)
+            step(profile)
             e1.record(stream)
             evs.append((e0, e1))
         torch.cuda.synchronize(dev)
@@ -200,6 +209,11 @@ def fusion_bench(args, rank, world, local, group):
 
     for _ in range(args.warmup):
         call.run(weights)
+    if group is None and not args.no_graph:
+        # one CUDA graph per step (K2, K1, finalize, K3 and the counter reset): the timed loop replays it
+        graph = call.capture(weights)
+        for _ in range(2):
+            step(False)
     with ClockSampler(local) as clk:
         ms = timed(args.steps, profile=False)
     clocks = clk.summary()
@@ -212,6 +226,7 @@ def fusion_bench(args, rank, world, local, group):
     st = call.check_status(per_tensor_raise=False)
     nonfinite = int((st == 2).sum())
     res = dict(ms=ms_max, ms_local=ms, kern_local=kern, kern_max=kmax, local_params=local_params,
+               launch=("one CUDA-graph replay per step (FusionCall.capture)" if graph is not None else "eager launches"),
                l2=("L2 flushed (512 MiB write) before every timed step; inputs "
                    f"{in_bytes / 2**20:.0f} MiB" if flush is not None else
                    f"inputs {in_bytes / 1e9:.0f} GB >> 126 MB L2; no flush needed"),
@@ -562,6 +577,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-grpo", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the timed fusion steps eagerly")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--json-out", default=None)
     args = ap.parse_args()
@@ -634,7 +650,7 @@ def main():
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-hash normal, SURVEY 8(d))",
         "config": {"workload": workload, "params": total, "tensors": fz["n_tensors"], "experts": N_EXPERTS,
                    "parallelism": f"param-range shards x{world}, NCCL all_reduce of norm partials",
-                   "l2": fz["l2"],
+                   "l2": fz["l2"], "launch": fz["launch"],
                    "dropout_mode": {1: "inline", 2: "bitmap"}.get(fz["dropout_mode"], "none")},
         "hbm_gbs_step": step_gbs, "hbm_frac_step": step_gbs / peak,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

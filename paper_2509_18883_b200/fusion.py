@@ -260,6 +260,19 @@ class FusionCall:
             self.counters.zero_()
         return self.norms().merge(weights, dtype_out)
 
+    def capture(self, weights: Sequence[float], dtype_out: torch.dtype | None = None) -> "torch.cuda.CUDAGraph":
+        """`run(weights)` captured once into a CUDA graph on the call's stream; `graph.replay()` inside
+        `torch.cuda.stream(call.stream)` repeats the whole step (same buffers) with one launch.  For
+        small, launch-bound fusions; single-process only (the sharded step has NCCL collectives)."""
+        if self.group is not None:
+            raise NotImplementedError("graph capture of the sharded step is not supported")
+        self.run(weights, dtype_out)  # allocates the lazily-sized buffers outside the capture
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            self.run(weights, dtype_out)
+        return g
+
     def _bitmap(self, s) -> None:
         """K2: keep bits for every (expert, within-tensor index < max extent) -- before K1, which
         counts the non-zero entries after dropout, and K3."""

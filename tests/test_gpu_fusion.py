@@ -268,3 +268,30 @@ def test_sharded_items_identical(cuda):
         for a, b in zip(r[1], results[0][1]):
             assert torch.equal(a.view(torch.int16), b.view(torch.int16))
         assert torch.equal(r[2], results[0][2])
+
+
+def test_graph_capture_replays_the_step(cuda):
+    """FusionCall.capture: the replayed graph gives the eager step's outputs and counters."""
+    from paper_2509_18883_b200 import fusion as F
+    base, experts = synth_state_dicts(mlp_dict_shapes(8), 3, seed=13, dtype_round=bf16_round)
+    names = list(base)
+    B = [torch.from_numpy(base[k].reshape(-1)).to(cuda, torch.bfloat16) for k in names]
+    E = [[torch.from_numpy(e[k].reshape(-1)).to(cuda, torch.bfloat16) for k in names] for e in experts]
+    pieces = [F.Piece(t, 0, B[t], [E[i][t] for i in range(3)], torch.empty_like(B[t])) for t in range(len(names))]
+    call = F.FusionCall(pieces, F.FusionLayout([b.numel() for b in B]), 3, F.FusionConfig(dropout_p=0.5, seed=3),
+                        stream=torch.cuda.Stream())
+    w = (1 / 3,) * 3
+    call.run(w)
+    torch.cuda.synchronize()
+    eager = [p.out.clone() for p in pieces]
+    cnt = call.counters.clone()
+    g = call.capture(w)
+    for p in pieces:
+        p.out.zero_()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(call.stream):
+        g.replay()
+    torch.cuda.synchronize()
+    for a, p in zip(eager, pieces):
+        assert torch.equal(a.view(torch.int16), p.out.view(torch.int16))
+    assert torch.equal(cnt, call.counters)
