@@ -78,8 +78,6 @@ def fusion_cases():
         for k, e in enumerate(es):
             cases[f"{dname}/expert{k}"] = e
         for cname, cfg in cfgs.items():
-            if dname == "bf16" and cname in ("none_noerase",):
-                continue
             taus = [fusion.task_vector(PT(e), PT(b)) for e in es]
             fused, st = fusion.fuse(PT(b), taus, cfg)
             key = f"{dname}/{cname}"

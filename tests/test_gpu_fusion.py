@@ -50,7 +50,7 @@ def test_fuse_kat_f64(cuda, golden_fusion, cname):
 
 
 @pytest.mark.parametrize("fast", ["1", "0"])
-@pytest.mark.parametrize("cname", ["default", "p05_s42", "p05_s42_sq", "p03_s7_t1_w", "p09_s3_none"])
+@pytest.mark.parametrize("cname", ["default", "p05_s42", "p05_s42_sq", "p03_s7_t1_w", "p09_s3_none", "none_noerase"])
 def test_fuse_bf16_exact(cuda, golden_fusion, cname, fast, monkeypatch):
     """bf16 in / bf16 out must equal RNE_bf16(reference f64 output) bit for bit."""
     monkeypatch.setenv("RLK_MERGE_FAST", fast)
