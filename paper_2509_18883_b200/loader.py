@@ -156,6 +156,25 @@ def plan_groups(numels: Sequence[int], n_experts: int, esize: int, budget_bytes:
     return groups
 
 
+def ring_placement(sizes: Sequence[int], cap: int) -> tuple[list[int], list[list[int]]]:
+    """Place groups of `sizes` elements one after another in a ring of `cap` (wrapping to 0 when a
+    group does not fit before the end).  Returns each group's offset and, per group, the earlier groups
+    whose space it overwrites (its H2D must wait for their D2H); a group is evicted by the first later
+    group that overlaps it."""
+    place, waits, live, head = [], [], [], 0
+    for gi, size in enumerate(sizes):
+        if size > cap:
+            raise ValueError(f"group {gi} ({size} elements) exceeds the ring ({cap})")
+        if head + size > cap:
+            head = 0
+        lo, hi = head, head + size
+        waits.append([j for j, a, b in live if a < hi and lo < b])
+        live = [(j, a, b) for j, a, b in live if not (a < hi and lo < b)] + [(gi, lo, hi)]
+        place.append(lo)
+        head = hi
+    return place, waits
+
+
 def _footprint(n: int, n_experts: int, esize: int) -> int:
     return (n + 63) // 64 * 64 * esize * (n_experts + 2)
 
@@ -182,19 +201,9 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
         raise ValueError("the largest tensor does not fit the device budget; raise the budget")
     # groups of at most half the ring, so that one can stream in while the previous one computes
     groups = plan_groups(numels, n_experts, esize, max(min(group_bytes, device_budget_bytes // 2), biggest * esize))
-    # ring placement, decided up front: offset of each group and the earlier groups it overwrites
-    place, waits, live, head = [], [], [], 0
-    for gi, group in enumerate(groups):
-        size = sum(_footprint(numels[t], n_experts, esize) for t in group) // esize
-        if head + size > cap:
-            head = 0
-        lo, hi = head, head + size
-        waits.append([j for j, a, b in live if a < hi and lo < b])
-        live = [(j, a, b) for j, a, b in live if not (a < hi and lo < b)] + [(gi, lo, hi)]
-        place.append(lo)
-        head = hi
-    ring = torch.empty(min(cap, max(p + sum(_footprint(numels[t], n_experts, esize) for t in g) // esize
-                                    for p, g in zip(place, groups))), dtype=dtype, device=dev)
+    sizes = [sum(_footprint(numels[t], n_experts, esize) for t in g) // esize for g in groups]
+    place, waits = ring_placement(sizes, cap)
+    ring = torch.empty(min(cap, max(p + z for p, z in zip(place, sizes))), dtype=dtype, device=dev)
     own_loader = loader is None
     loader = loader or HostLoader()
     h2d_s, comp_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
