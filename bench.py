@@ -654,7 +654,8 @@ def main():
                    "dropout_mode": {1: "inline", 2: "bitmap"}.get(fz["dropout_mode"], "none")},
         "hbm_gbs_step": step_gbs, "hbm_frac_step": step_gbs / peak,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "frac": achieved / peak, "frac_of_8tbs_spec": achieved / 8000.0, "traffic": traffic,
+                     "peak_source": peak_src,
                      "bytes_per_param": kb[dom], "kernels_ms": fz["kern_local"]},
         "clocks": fz["clocks"],
         "gpu_launches": fz["launches_per_step"] * args.steps,

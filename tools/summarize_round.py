@@ -79,6 +79,12 @@ for rep, out in (("fusion_full", "ncu_fusion_summary"), ("grpo_full", "ncu_grpo_
                 "rlk_fusion_mask_bitmap" if "k_mask" in name else name.split("(")[0]
             traffic.setdefault(key, []).append(b)
             txt.append(f"    {'dram bytes read + write':60s} {b:18.0f} byte")
+            dur = float(d["gpu__time_duration.sum"].replace(",", ""))
+            dur_s = dur * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(
+                u.get("gpu__time_duration.sum", "ms"), 1e-3)
+            gbs = b / dur_s / 1e9
+            txt.append(f"    {'achieved DRAM GB/s (ncu, isolated launch)':60s} {gbs:18.1f} GB/s "
+                       f"= {gbs / 8000 * 100:.1f}% of the 8 TB/s spec, {gbs / 6546.6 * 100:.1f}% of the measured copy peak")
         txt.append("")
     (dst / f"{tag}_{out}.txt").write_text("\n".join(txt))
 raw_t = {k: v for k, v in traffic.items()}
