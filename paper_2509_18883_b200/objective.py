@@ -340,11 +340,21 @@ def grpo_forward_backward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConf
 
 
 class GRPOTokenLoss(torch.autograd.Function):
-    """Autograd wrapper: forward returns J (maximised objective); backward runs K5."""
+    """Autograd wrapper: forward returns J (maximised objective); backward runs K5.
+
+    With `fused_scale` set (the d(loss)/dJ the caller will back-propagate, e.g. -1.0 for
+    loss = -J), the forward runs the fused loss+gradient kernel -- one read of the logits instead of
+    K4 now and K5 later -- and keeps `fused_scale * dJ/dlogits`; backward returns it when grad_out
+    equals fused_scale (one scalar read), and otherwise recomputes with K5."""
 
     @staticmethod
-    def forward(ctx, logits, batch: GRPOBatch, clip: ClipConfig):
-        fwd = grpo_forward(logits, batch, clip)
+    def forward(ctx, logits, batch: GRPOBatch, clip: ClipConfig, fused_scale=None):
+        ctx.saved_grad = None
+        if fused_scale is not None and logits.requires_grad:
+            fwd, g = grpo_forward_backward(logits, batch, clip, grad_scale=float(fused_scale))
+            ctx.saved_grad, ctx.fused_scale = g, float(fused_scale)
+        else:
+            fwd = grpo_forward(logits, batch, clip)
         ctx.save_for_backward(logits)
         ctx.batch, ctx.fwd = batch, fwd
         return fwd.objective
@@ -352,12 +362,17 @@ class GRPOTokenLoss(torch.autograd.Function):
     @staticmethod
     def backward(ctx, grad_out):
         (logits,) = ctx.saved_tensors
+        if ctx.saved_grad is not None and float(grad_out) == ctx.fused_scale:
+            g, ctx.saved_grad = ctx.saved_grad, None
+            return g.to(logits.dtype), None, None, None
         g = grpo_backward(logits, ctx.batch, ctx.fwd, grad_out.to(torch.float64))
-        return g, None, None
+        return g, None, None, None
 
 
-def grpo_token_objective(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = ClipConfig()) -> torch.Tensor:
-    return GRPOTokenLoss.apply(logits, batch, clip)
+def grpo_token_objective(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = ClipConfig(),
+                         fused_scale: float | None = None) -> torch.Tensor:
+    """J with autograd support; see GRPOTokenLoss for `fused_scale` (one-read loss + gradient)."""
+    return GRPOTokenLoss.apply(logits, batch, clip, fused_scale)
 
 
 def token_logprobs(logits2d: torch.Tensor, tokens: Sequence[int], temperature: float = 1.0,

@@ -115,6 +115,15 @@ def test_autograd_and_bf16_grad(cuda):
     fwd = O.grpo_forward(lg.detach(), b)
     ref = O.grpo_backward(lg.detach(), b, fwd, grad_dtype=torch.float32) * -2.0
     np.testing.assert_allclose(lg.grad.float().cpu().numpy(), ref.cpu().numpy(), rtol=1e-2, atol=1e-9)
+    # fused mode: loss = -J with fused_scale = -1 returns the one-read gradient; a different grad_out
+    # falls back to K5
+    scale = float(np.abs(ref.cpu().numpy()).max())
+    for mult, fused in ((-1.0, -1.0), (3.0, -1.0)):
+        lg2 = torch.from_numpy(logits).to(cuda, torch.bfloat16).requires_grad_(True)
+        (mult * O.grpo_token_objective(lg2, b, fused_scale=fused)).backward()
+        ref2 = O.grpo_backward(lg.detach(), b, fwd, grad_dtype=torch.float32) * mult
+        np.testing.assert_allclose(lg2.grad.float().cpu().numpy(), ref2.cpu().numpy(), rtol=0,
+                                   atol=1e-2 * scale * abs(mult) / 2 + 1e-12)
 
 
 def test_f64_finite_difference(cuda):
