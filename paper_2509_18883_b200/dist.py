@@ -6,8 +6,9 @@ items from its own start) is split into world-size contiguous ranges balanced by
 range of the output.  The one exchange is the all_reduce of the f64 norm partials between K1 and
 finalize -- every (item, expert) slot is produced by exactly one rank and is exactly zero elsewhere,
 so the NCCL sum is exact and the norms (hence scales, masks, erase decisions and outputs) are
-bit-identical at every world size.  The dropout keep bitmap is drawn 1/world per rank and
-all-gathered (one collective per expert row), so no rank draws the whole embedding-sized rows.  FusionStats counters are summed by a second (int64) all_reduce
+bit-identical at every world size.  With `FusionLayout.partition_striped` (the default here) the
+embedding-sized tensors are cut into one stripe per rank, so each rank draws only the dropout keep
+bits of its own index ranges and no bitmap crosses GPUs.  FusionStats counters are summed by a second (int64) all_reduce
 only when statistics are requested.
 
 The GRPO loss shards by response; per-group token-term sums are all-reduced (objective.grpo_forward).
@@ -40,29 +41,9 @@ def allreduce_counts(counts: torch.Tensor, group) -> torch.Tensor:
     return counts
 
 
-def allgather_bitmap_rows(bitmap2d: torch.Tensor, words_per_rank: int, group) -> torch.Tensor:
-    """All-gather of a [N, world * words_per_rank] keep bitmap whose rank-r column slice
-    [r * words_per_rank, (r + 1) * words_per_rank) each rank has drawn, into the same buffer (one
-    collective per expert row)."""
-    import torch.distributed as dist
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
-    lo = rank * words_per_rank
-    for i in range(bitmap2d.shape[0]):
-        row = bitmap2d[i]
-        mine = row[lo:lo + words_per_rank]
-        if row.is_cuda:
-            # a separate send buffer (an in-place all-gather would alias the receive buffer)
-            dist.all_gather_into_tensor(row, mine.clone(), group=group)
-        else:  # gloo: list form
-            parts = [torch.empty_like(mine) for _ in range(world)]
-            dist.all_gather(parts, mine.clone(), group=group)
-            row.copy_(torch.cat(parts))
-    return bitmap2d
-
-
 def rank_pieces(layout: FusionLayout, world: int, rank: int) -> list[tuple[int, int, int]]:
-    """This rank's (tensor, lo, hi) element ranges."""
-    return layout.partition(world, rank)
+    """This rank's (tensor, lo, hi) element ranges (big tensors striped over the ranks)."""
+    return layout.partition_striped(world, rank)
 
 
 def shard_state_dicts(base: Mapping[str, torch.Tensor], experts: Sequence[Mapping[str, torch.Tensor]], world: int,
@@ -75,7 +56,7 @@ def shard_state_dicts(base: Mapping[str, torch.Tensor], experts: Sequence[Mappin
     layout = FusionLayout([base[k].numel() for k in names])
     dev = torch.device("cuda", torch.cuda.current_device())
     pieces = []
-    for t, lo, hi in layout.partition(world, rank):
+    for t, lo, hi in layout.partition_striped(world, rank):
         name = names[t]
         b = base[name].reshape(-1)[lo:hi].to(dev).contiguous()
         es = [e[name].reshape(-1)[lo:hi].to(dev).contiguous() for e in experts]

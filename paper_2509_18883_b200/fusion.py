@@ -109,6 +109,45 @@ class FusionLayout:
             self._dev[key] = _upload(self.tensor_items.astype(np.uint32).view(np.int32), device, stream)
         return self._dev[key]
 
+    def partition_striped(self, world: int, rank: int) -> list[tuple[int, int, int]]:
+        """Like `partition`, but every tensor of at least max(ITEM * world, max numel / 4) elements (the
+        embedding-sized ones) is cut into `world` item-aligned stripes, one per rank, and the remaining
+        tensors' items are split into contiguous ranges balanced by element count.  A rank's pieces
+        then read the dropout keep bits of their own index ranges only (the stripes of equally sized
+        big tensors share one range), so each rank draws its own bits and no bitmap exchange is needed.
+        Returns [(tensor, lo, hi)] in tensor order (lo a multiple of ITEM)."""
+        if world < 1 or not 0 <= rank < world:
+            raise ValueError(f"bad rank {rank} of {world}")
+        if not self.numels:
+            return []
+        big_min = max(ITEM * world, max(self.numels) / 4)
+        out: list[tuple[int, int, int]] = []
+        small = []
+        for t, n in enumerate(self.numels):
+            if n >= big_min:
+                items = (n + ITEM - 1) // ITEM
+                a, b = items * rank // world, items * (rank + 1) // world
+                if b > a:
+                    out.append((t, a * ITEM, min(b * ITEM, n)))
+            else:
+                for k in range((n + ITEM - 1) // ITEM):
+                    small.append((t, k * ITEM, min(ITEM, n - k * ITEM)))
+        if small:
+            starts = np.cumsum([0] + [x[2] for x in small])
+            tot = int(starts[-1])
+            bounds = [int(np.searchsorted(starts, tot * r / world, side="left")) for r in range(world + 1)]
+            bounds[-1] = len(small)
+            for t, lo, n in small[bounds[rank]:bounds[rank + 1]]:
+                out.append((t, lo, lo + n))
+        out.sort()
+        merged: list[tuple[int, int, int]] = []
+        for t, lo, hi in out:
+            if merged and merged[-1][0] == t and merged[-1][2] == lo:
+                merged[-1] = (t, merged[-1][1], hi)
+            else:
+                merged.append((t, lo, hi))
+        return merged
+
     def partition(self, world: int, rank: int) -> list[tuple[int, int, int]]:
         """Rank `rank`'s contiguous share of the global item list, balanced by element count.
 
@@ -162,6 +201,18 @@ def _upload(arr: np.ndarray, device, stream=None) -> torch.Tensor:
         return host.to(device)
     with torch.cuda.stream(stream):
         return host.pin_memory().to(device, non_blocking=True)
+
+
+def needed_bit_ranges(spans: Sequence[tuple[int, int]]) -> list[tuple[int, int]]:
+    """Union of element index ranges [lo, hi) as sorted disjoint ranges with lo rounded down and hi
+    rounded up to 32 (whole bitmap words)."""
+    out: list[tuple[int, int]] = []
+    for lo, hi in sorted((lo // 32 * 32, (hi + 31) // 32 * 32) for lo, hi in spans if hi > lo):
+        if out and lo <= out[-1][1]:
+            out[-1] = (out[-1][0], max(out[-1][1], hi))
+        else:
+            out.append((lo, hi))
+    return out
 
 
 class _Plan:
@@ -278,10 +329,10 @@ class FusionCall:
         counts the non-zero entries after dropout, and K3."""
         if self.dropout_mode != 2:
             return
-        world, rank = 1, 0
+        world = 1
         if self.group is not None:
             import torch.distributed as dist
-            world, rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+            world = dist.get_world_size(self.group)
         seeds = (L.C.c_uint64 * self.n)(*self.seeds)
         if world == 1:
             n_bits = ((self.plan.max_extent + 8191) // 8192) * 8192
@@ -290,18 +341,16 @@ class FusionCall:
             self._launch("rlk_fusion_mask_bitmap", seeds, self.n, self.thresh, n_bits, L.ptr(self.bitmap),
                          self.words_per_row, s)
             return
-        # sharded: every rank draws 1/world of each row (the rows span the layout's largest tensor, the
-        # same on every rank) and the slices are all-gathered -- instead of the ranks holding an
-        # embedding-sized piece each drawing the whole rows
+        # sharded: the rows span the layout's largest tensor (the same row pitch on every rank), but a
+        # rank draws only the index ranges its own pieces read -- with `partition_striped` the
+        # embedding-sized tensors contribute one stripe each, so no rank draws whole rows and no
+        # bitmap crosses GPUs
         n_bits = ((max(self.layout.numels) + 8191) // 8192) * 8192
-        wc = ((n_bits // 32 + world - 1) // world + 3) // 4 * 4  # words per rank slice, 16-byte multiple
-        self.words_per_row = wc * world
+        self.words_per_row = n_bits // 32
         self._alloc_bitmap()
-        lo, hi = min(rank * wc * 32, n_bits), min((rank + 1) * wc * 32, n_bits)
-        self._launch("rlk_fusion_mask_bitmap_range", seeds, self.n, self.thresh, lo, hi, L.ptr(self.bitmap),
-                     self.words_per_row, s)
-        from .dist import allgather_bitmap_rows
-        allgather_bitmap_rows(self.bitmap.view(self.n, self.words_per_row), wc, self.group)
+        for lo, hi in needed_bit_ranges([(p.j0, p.j0 + p.numel) for p in self.pieces]):
+            self._launch("rlk_fusion_mask_bitmap_range", seeds, self.n, self.thresh, lo, min(hi, n_bits),
+                         L.ptr(self.bitmap), self.words_per_row, s)
 
     def _alloc_bitmap(self) -> None:
         if self.bitmap is None or self.bitmap.numel() != self.n * self.words_per_row:

@@ -226,8 +226,11 @@ def test_fast_path_equals_exact_path_random(cuda, monkeypatch):
         assert torch.equal(outs[0][1], outs[1][1]), cfg
 
 
-def test_sharded_items_identical(cuda):
-    """Pieces split over 2/4 'ranks' (item-aligned) give bit-identical norms, outputs and counters."""
+@pytest.mark.parametrize("striped", [False, True])
+def test_sharded_items_identical(cuda, striped, monkeypatch):
+    """Pieces split over 2/4 'ranks' (item-aligned) give bit-identical norms, outputs and counters.
+    Striped: each rank's FusionCall takes the sharded keep-bitmap path (draws only the index ranges
+    its pieces read, `needed_bit_ranges`), with the world size reported by a stand-in group."""
     from paper_2509_18883_b200 import fusion as F
     base, experts = synth_state_dicts({"a": (3000, 517), "b": (70001,), "c": (1024, 1024)}, 3, seed=3,
                                       dtype_round=bf16_round)
@@ -245,11 +248,19 @@ def test_sharded_items_identical(cuda):
         calls = []
         for rank in range(world):
             pieces = [F.Piece(t, lo, B[t][lo:hi], [E[i][t][lo:hi] for i in range(3)], outs[t][lo:hi])
-                      for t, lo, hi in layout.partition(world, rank)]
+                      for t, lo, hi in (layout.partition_striped if striped else layout.partition)(world, rank)]
             c = F.FusionCall(pieces, layout, 3, cfg)
             c.partials = partials
             from paper_2509_18883_b200 import _lib as L
-            c._bitmap(L.stream_handle())
+            if striped and world > 1:
+                import torch.distributed as dist
+                monkeypatch.setattr(dist, "get_world_size", lambda group=None, w=world: w)
+                c.group = "stand-in"
+                c._bitmap(L.stream_handle())
+                c.group = None
+                monkeypatch.undo()
+            else:
+                c._bitmap(L.stream_handle())
             L.call("rlk_fusion_sumsq", L.C.byref(c.plan.c), 3, L.RLK_BF16, 0, L.ptr(partials), L.ptr(c.counters),
                    c.dropout_mode, (L.C.c_uint64 * 3)(*c.seeds), c.thresh, L.ptr(c.bitmap), c.words_per_row,
                    L.stream_handle())

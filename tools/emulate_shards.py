@@ -1,8 +1,8 @@
 """Per-rank work of the sharded config-3 fusion, run one rank at a time on ONE GPU (no collectives):
-for world = 1, 2, 4, 8 and every rank, the rank's pieces (FusionLayout.partition) go through K1,
-finalize and K3, and the rank's 1/world slice of the keep-bitmap rows through K2 (the all-gather
-that completes the rows, and the partials all-reduce, are not timed here).  Prints the slowest rank
-per world size and the implied strong-scaling efficiency of the compute."""
+for world = 1, 2, 4, 8 and every rank, the rank's pieces (FusionLayout.partition_striped, or
+partition with --contiguous) go through K2 (only the keep-bit ranges the rank reads), K1, finalize
+and K3; the partials all-reduce is not timed here.  Prints the slowest rank per world size and the
+implied strong-scaling efficiency of the compute."""
 import json
 import statistics
 import sys
@@ -16,6 +16,7 @@ from paper_2509_18883_b200 import fusion as F  # noqa: E402
 from paper_2509_18883_b200.layouts import LAYOUTS, fill_synthetic, numel  # noqa: E402
 
 layout_name = sys.argv[1] if len(sys.argv) > 1 else "llama8b"
+STRIPED = "--contiguous" not in sys.argv
 shapes = LAYOUTS[layout_name]()
 numels = [numel(s) for s in shapes.values()]
 layout = F.FusionLayout(numels)
@@ -29,27 +30,25 @@ n_bits = ((max(numels) + 8191) // 8192) * 8192
 def time_rank(world, rank, reps=5):
     pieces = []
     with torch.cuda.stream(s):
-        for t, lo, hi in layout.partition(world, rank):
+        for t, lo, hi in (layout.partition_striped if STRIPED else layout.partition)(world, rank):
             n = hi - lo
             b = torch.empty(n, dtype=torch.bfloat16, device=dev)
             es = [torch.empty(n, dtype=torch.bfloat16, device=dev) for _ in range(3)]
             fill_synthetic(b, es, t, j0=lo, stream=s)
             pieces.append(F.Piece(t, lo, b, es, torch.empty(n, dtype=torch.bfloat16, device=dev)))
     call = F.FusionCall(pieces, layout, 3, cfg, stream=s)
-    # the rank's share of the bitmap rows, as the sharded K2 draws them
-    wc = ((n_bits // 32 + world - 1) // world + 3) // 4 * 4
-    call.words_per_row = wc * world
+    call.words_per_row = n_bits // 32
     call._alloc_bitmap()
     seeds = (L.C.c_uint64 * 3)(*call.seeds)
-    lo_b, hi_b = min(rank * wc * 32, n_bits), min((rank + 1) * wc * 32, n_bits)
-
-    call._bitmap = lambda *_a, **_k: None  # K2 is the explicit range launch below
+    ranges = F.needed_bit_ranges([(p.j0, p.j0 + p.numel) for p in pieces])  # what the sharded K2 draws
+    call._bitmap = lambda *_a, **_k: None  # K2 is the explicit range launches below
 
     def step():
         with torch.cuda.stream(s):
             call.counters.zero_()
-        L.call("rlk_fusion_mask_bitmap_range", seeds, 3, call.thresh, lo_b, hi_b, L.ptr(call.bitmap),
-               call.words_per_row, L.stream_handle(s))
+        for lo_b, hi_b in ranges:
+            L.call("rlk_fusion_mask_bitmap_range", seeds, 3, call.thresh, lo_b, min(hi_b, n_bits), L.ptr(call.bitmap),
+                   call.words_per_row, L.stream_handle(s))
         call.norms().merge(w)  # K1 + finalize + K3 (outputs not checked: timing only)
 
     for _ in range(2):
