@@ -609,9 +609,10 @@ __device__ __forceinline__ uint32_t fast_opp_bits(float b, const float* x, uint3
     const float d = delta ? x[i] : fmaf(b, -1.f, x[i]);
     k[i] = __fmul_rn(d, ((keep >> i) & 1u) ? sr32[i] : 0.f);
   }
+  // the same operations as the packed phase 1: sum mode adds, squared mode k0|k0| then fused k_i|k_i| + v
   float v = erase_mode == 1 ? k[0] : __fmul_rn(k[0], fabsf(k[0]));
 #pragma unroll
-  for (int i = 1; i < N; ++i) v = __fadd_rn(v, erase_mode == 1 ? k[i] : __fmul_rn(k[i], fabsf(k[i])));
+  for (int i = 1; i < N; ++i) v = erase_mode == 1 ? __fadd_rn(v, k[i]) : __fmaf_rn(k[i], fabsf(k[i]), v);
   const float sg = copysignf(1.f, v);
   uint32_t m = 0;
 #pragma unroll
@@ -758,6 +759,17 @@ __device__ __forceinline__ float2 bf16x2_minus_f32(uint32_t w, float2 b) {
   asm("{\n .reg .b16 lo, hi;\n mov.b32 {lo, hi}, %2;\n sub.rn.f32.bf16 %0, lo, %3;\n sub.rn.f32.bf16 %1, hi, %4;\n}"
       : "=f"(r.x), "=f"(r.y)
       : "r"(w), "f"(b.x), "f"(b.y));
+  return r;
+}
+// min that propagates NaN (min.NaN.f32): a NaN guard margin must force the exact path
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmin3_nan(float a, float b, float c) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
 // +-1.0f with the sign of x (one LOP3)
@@ -971,18 +983,26 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
           const float2 mid = make_float2(mid_of(y2.x), mid_of(y2.y));
           const float2 dm = __fadd2_rn(y2, make_float2(-mid.x, -mid.y));
           const float2 g2 = __ffma2_rn(make_float2(-0x1p-20f, -0x1p-20f), S2, make_float2(fabsf(dm.x), fabsf(dm.y)));
-          gm[2 * p] = fminf(g1.x, g2.x);
-          gm[2 * p + 1] = fminf(g1.y, g2.y);
+          // The bounds above are relative (normal-range rounding).  They also hold when S >= 2^-90: a
+          // subnormal intermediate needs deltas below 2^-100, hence a base below 2^-93, hence S < 2^-90
+          // (squared vote: k^2 must stay normal, i.e. |k| >= 2^-63, which S >= 2^-38 guarantees with
+          // sr >= 2^-16).  g3 < 0 flags 0 < S < that floor (S == 0 is an all-zero column: exact);
+          // overflow to inf makes a margin NaN, which the NaN-propagating minimum turns into a fallback.
+          constexpr float kInvFloor = ERASE == 2 ? 0x1p38f : 0x1p90f;
+          // g3 = max(S / floor - 1, -S): < 0 exactly for 0 < S < floor (-0 for S == 0)
+          const float2 g3a = __ffma2_rn(S2, make_float2(kInvFloor, kInvFloor), make_float2(-1.f, -1.f));
+          gm[2 * p] = fmin3_nan(g1.x, g2.x, fmaxf(g3a.x, -S2.x));
+          gm[2 * p + 1] = fmin3_nan(g1.y, g2.y, fmaxf(g3a.y, -S2.y));
           __nv_bfloat162 p2 = __floats2bfloat162_rn(y2.x, y2.y);
           outw[p] = *reinterpret_cast<uint32_t*>(&p2);
         }
         float gmin = gm[0];
 #pragma unroll
-        for (int e = 1; e < kFastElems; ++e) gmin = fminf(gmin, gm[e]);
+        for (int e = 1; e < kFastElems; ++e) gmin = fmin_nan(gmin, gm[e]);
         uint32_t slowm = 0;
-        if (gmin < 0.f) {
+        if (!(gmin >= 0.f)) {  // negative or NaN
 #pragma unroll
-          for (int e = 0; e < kFastElems; ++e) slowm |= (uint32_t)(gm[e] < 0.f) << e;
+          for (int e = 0; e < kFastElems; ++e) slowm |= (uint32_t)(!(gm[e] >= 0.f)) << e;
         }
         slowbits |= slowm << jit;
         FastVec::store(outp + out_base + le, outw);

@@ -306,3 +306,46 @@ def test_graph_capture_replays_the_step(cuda):
     for a, p in zip(eager, pieces):
         assert torch.equal(a.view(torch.int16), p.out.view(torch.int16))
     assert torch.equal(cnt, call.counters)
+
+
+def test_fast_path_adversarial_values(cuda, monkeypatch):
+    """The certified f32x2 merge against the reference-order f64 merge (bit-identical) and the oracle on
+    bf16 data built to stress the guards: magnitudes from 1e-30 to 1e30 in one tensor, exact zeros of
+    both signs, bf16 subnormals, experts of opposite sign to the base, exact vote ties and deltas that
+    cancel across experts."""
+    from paper_2509_18883_b200 import fusion as F
+    g = np.random.default_rng(21)
+    n = 1 << 18
+    mag = 10.0 ** g.uniform(-30, 30, n)
+    base = bf16_round(mag * g.choice([-1.0, 1.0], n))
+    base[g.random(n) < 0.05] = 0.0
+    base[g.random(n) < 0.02] = -0.0
+    base[g.random(n) < 0.01] = bf16_round(np.full(1, 1e-39))[0]  # subnormal
+    experts = []
+    for i in range(3):
+        e = bf16_round(base * (1 + g.normal(0, 0.01 * (i + 1), n)))
+        flip = g.random(n) < 0.1
+        e[flip] = bf16_round(-base[flip] * 0.5)  # opposite sign to the base
+        same = g.random(n) < 0.1
+        e[same] = base[same]  # zero deltas
+        experts.append(e)
+    # exact ties: expert 2's delta cancels expert 0's and expert 1 has none
+    tie = g.random(n) < 0.05
+    experts[1][tie] = base[tie]
+    experts[2][tie] = bf16_round(2 * base[tie] - experts[0][tie])
+    bt = torch.from_numpy(base).to(cuda, torch.bfloat16)
+    ets = [torch.from_numpy(e).to(cuda, torch.bfloat16) for e in experts]
+    for cfgkw in (dict(dropout_p=0.5, seed=4), dict(target_norm=None, dropout_p=0.5, seed=4),
+                  dict(erase_weighting="squared", merge_weights=(0.5, 0.3, 0.2))):
+        outs = []
+        for fast in ("1", "0"):
+            monkeypatch.setenv("RLK_MERGE_FAST", fast)
+            o, rep = F.fuse_state_dict({"w": bt}, [{"w": e} for e in ets], F.FusionConfig(**cfgkw))
+            outs.append((o["w"].clone(), rep.call.counters.clone()))
+        assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16)), cfgkw
+        assert torch.equal(outs[0][1], outs[1][1]), cfgkw
+        b64 = bt.float().double().cpu().numpy()
+        ref, st = OF.fuse(b64, [e.float().double().cpu().numpy() for e in ets], **cfgkw)
+        got = outs[0][0].view(torch.int16).cpu().numpy().view(np.uint16)
+        assert int((got != rne_bf16_bits(ref)).sum()) == 0, cfgkw
+        assert list(rep.stats("w").erased_counts) == st["erased"], cfgkw
