@@ -288,16 +288,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         st_async_peer(mapa(smem_u32(&slot[p]), peer), M, S, mapa(smem_u32(&xbar[p]), peer));
         mbar_wait(&xbar[p], ph[p]);
         const float2 o = slot[p];
-        // combine and run the epilogue (objective.py:243-248, 277-279) in f32 on the MUFU (ex2 / lg2).
+        // combine and run the epilogue (objective.py:243-248, 277-279) in float64, like K4's: this
+        // warp is off the consumers' critical path, so the precise exp / log cost nothing (an f32
+        // epilogue loses ~1e-5 absolute in logp = z/T - lse when |z/T| reaches hundreds).
         // Both CTAs compute the same numbers; rank 0 writes the per-token outputs.
         const float Mm = fmaxf(M, o.x);
-        float Sf = 0.f;
-        if (M != -INFINITY) Sf += S * ex2f_approx((M - Mm) * c);
-        if (o.x != -INFINITY) Sf += o.y * ex2f_approx((o.x - Mm) * c);
-        const float inv_t = (float)(1.0 / T);
-        float lg2s;
-        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg2s) : "f"(Sf));
-        const float lse = Mm * inv_t + lg2s * 0.69314718f;  // ln-sum-exp of z / T
+        double Sd = 0.0;
+        if (M != -INFINITY) Sd += (double)S * exp2(((double)M - (double)Mm) * (double)c);
+        if (o.x != -INFINITY) Sd += (double)o.y * exp2(((double)o.x - (double)Mm) * (double)c);
+        const double lse = (double)Mm / T + log(Sd);  // ln-sum-exp of z / T
         double cf = 0.0;
         if (tok < 0 || (uint64_t)tok >= a.vocab) {
           if (rank == 0) {
@@ -308,22 +307,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
             a.coef[row] = 0.0;
           }
         } else {
-          const float logp = (float)zt * inv_t - lse;
-          const float lt = (float)lt64, li = (float)li64;
-          const float r = ex2f_approx((logp - lt) * 1.44269504f);
-          const float w = fminf(ex2f_approx((lt - li) * 1.44269504f), (float)a.clip.tis_cap);
-          const TripletF tv = triplet_f((double)r, adv, a.clip);
-          cf = nrm * (double)w * tv.slope * (double)r / T;
+          const double logp = zt / T - lse;
+          const double r = exp(logp - lt64);
+          const double w = fmin(exp(lt64 - li64), a.clip.tis_cap);
+          const TripletF tv = triplet_f(r, adv, a.clip);
+          cf = nrm * w * tv.slope * r / T;
           if (rank == 0) {
             if (!isfinite(logp)) atomicOr(a.flags, 1);
             if (a.logp) a.logp[row] = logp;
             if (a.lse) a.lse[row] = lse;
-            a.term[row] = (double)w * tv.value;
+            a.term[row] = w * tv.value;
             a.coef[row] = cf;
           }
         }
         bcast[p * 4 + 0] = (float)(cf * a.grad_scale);
-        bcast[p * 4 + 1] = -lse * 1.44269504f;
+        bcast[p * 4 + 1] = (float)(-lse * kLog2eF);
         mbar_arrive(&cready[p]);
       }
       ph[p] ^= 1u;

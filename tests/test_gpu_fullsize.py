@@ -117,8 +117,8 @@ def test_fullsize_grpo_config5_chunk(cuda):
     b = O.GRPOBatch.pack(toks, lt, li, [0, T, R], adv, [1, 1], 2, T, temperature=0.7, device=cuda)
     fwd = O.grpo_forward(lg, b)
     fused, grad = O.grpo_forward_backward(lg, b)
-    assert float(fused.objective) == pytest.approx(float(fwd.objective), rel=1e-5)
-    np.testing.assert_allclose(fused.coef.cpu().numpy(), fwd.coef.cpu().numpy(), rtol=1e-4, atol=1e-14)
+    assert float(fused.objective) == pytest.approx(float(fwd.objective), rel=2e-6)
+    np.testing.assert_allclose(fused.coef.cpu().numpy(), fwd.coef.cpu().numpy(), rtol=2e-6, atol=1e-14)
     rows = np.unique(np.concatenate([[0, T - 1, T, R - 1], g.integers(0, R, 28)]))
     z = lg[torch.from_numpy(rows).to(cuda)].float().double().cpu().numpy()
     clip = dict(eps_neg_low=0.2, eps_pos_high=0.2, eps_neg_high=3.0, tis_cap=2.0, guard_positive=True)
