@@ -92,3 +92,28 @@ def test_ragged_tails_and_item_boundaries(cuda):
         ref, st = OF.fuse(base["t"], [e["t"] for e in experts], **cfgkw)
         _check(outs["t"], ref, torch.bfloat16, f"n={n}")
         assert list(rep.stats("t").erased_counts) == st["erased"], n
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_generic_path_extreme_magnitudes(cuda, dtype):
+    """The reference-order f64 merge on f32 / f64 data spanning 1e-30..1e30, signed zeros and
+    opposite-sign experts: f32 output = RN_f32(reference), f64 output within 1e-12."""
+    from paper_2509_18883_b200 import fusion as F
+    g = np.random.default_rng(31)
+    n = 40000
+    base = 10.0 ** g.uniform(-30, 30, n) * g.choice([-1.0, 1.0], n)
+    base[g.random(n) < 0.05] = 0.0
+    experts = []
+    for i in range(3):
+        e = base * (1 + g.normal(0, 0.01 * (i + 1), n))
+        flip = g.random(n) < 0.1
+        e[flip] = -base[flip] * 0.5
+        experts.append(e)
+    rnd = _round_for(dtype)
+    base, experts = rnd(base), [rnd(e) for e in experts]
+    to = lambda a: {"w": torch.from_numpy(a).to(cuda, dtype)}
+    for cfgkw in (dict(dropout_p=0.5, seed=2), dict(erase_weighting="squared", target_norm=None)):
+        outs, rep = F.fuse_state_dict(to(base), [to(e) for e in experts], F.FusionConfig(**cfgkw))
+        ref, st = OF.fuse(base, experts, **cfgkw)
+        _check(outs["w"], ref, dtype, str(cfgkw))
+        assert list(rep.stats("w").erased_counts) == st["erased"]
