@@ -913,14 +913,21 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
           const uint32_t bw = bw4.w[p];
           const float2 b2 = make_float2(bf16_lo(bw), bf16_hi(bw));
           float2 k2[N];
-          float2 aa = make_float2(0.f, 0.f);
 #pragma unroll
           for (int i = 0; i < N; ++i) {
             uint32_t xw = xw4[i].w[p];
             if (DROP) xw = select_halves(xw, bw, prmt_sign(spread[i], p == 0 ? 0x9988u : 0xBBAAu));
             const float2 d2 = bf16x2_minus_f32(xw, b2);
             k2[i] = __fmul2_rn(d2, make_float2(sr32[i], sr32[i]));
-            aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
+          }
+          // sum |k| (|k0| + |k1| first: the abs modifiers ride on one FADD2, no add of zero)
+          float2 aa;
+          if constexpr (N == 1) {
+            aa = make_float2(fabsf(k2[0].x), fabsf(k2[0].y));
+          } else {
+            aa = __fadd2_rn(make_float2(fabsf(k2[0].x), fabsf(k2[0].y)), make_float2(fabsf(k2[1].x), fabsf(k2[1].y)));
+#pragma unroll
+            for (int i = 2; i < N; ++i) aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
           }
           float2 y2, g1 = make_float2(1.f, 1.f);
           if constexpr (kErase) {
