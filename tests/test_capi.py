@@ -67,3 +67,15 @@ def test_more_argument_checks_before_any_device_work():
     with pytest.raises(ValueError, match="multiple of 16"):
         L.call("rlk_grpo_fused_bf16", 16, 4, 100, 100, None, 16, 8, 8, 8, 8, 8, 8, 8, ctypes.byref(clip), 1.0, None,
                None, 8, 8, 8, 16, 100, None)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: with the sm_100a library absent, the first kernel call raises RlkError."""
+    import os
+    import subprocess
+    import sys
+    code = ("from paper_2509_18883_b200 import _lib as L\n"
+            "try:\n    L.lib()\nexcept L.RlkError as e:\n    print('RAISED', e)\n")
+    env = dict(os.environ, RLK_LIB_PATH=str(tmp_path / "absent.so"), RLK_AUTOBUILD="0")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, env=env, timeout=300)
+    assert "RAISED" in out.stdout and "no CPU fallback" in out.stdout, out.stdout + out.stderr
