@@ -113,13 +113,13 @@ int rlk_fusion_mask_bitmap_range(const uint64_t* child_seeds, int n_experts, uin
  * counters: device [n_tensors * 2N] u64, accumulated (caller zeroes): K3 adds the entries erased at
  * [t*2N + N + i] (the non-zero-after-dropout counts at [t*2N + i] come from K1).
  * bf16 -> bf16 with N <= 4 and dropout_mode 0/2 runs the f32x2 fast kernel with certified guards
- * (bit-identical to the f64 path); environment variable RLK_MERGE_FAST=0 forces the f64 path (a test
- * hook: the results are the same either way). */
+ * (bit-identical to the f64 path); exact_path = 1 forces the reference-order f64 kernel instead (the
+ * results are the same either way; the parity tests compare the two). */
 int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, int dtype_out,
                      int delta_mode, const double* scale, const double* weights, int dropout_mode,
                      const uint64_t* child_seeds, uint64_t thresh, double keep_prob,
                      const uint32_t* bitmap, uint64_t words_per_row, int erase_mode,
-                     unsigned long long* counters, void* stream);
+                     unsigned long long* counters, int exact_path, void* stream);
 
 /* GRPO token objective over packed rows (K4).  Token r reads logits row row_index[r] (or r when
  * row_index is NULL), row_stride elements between rows, vocab V.  Per token: token id, behaviour

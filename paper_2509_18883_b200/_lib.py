@@ -55,7 +55,7 @@ SIGNATURES = {
     "rlk_fusion_mask_bitmap": (_I, [_P, _I, _U64, _U64, _P, _U64, _P]),
     "rlk_fusion_mask_bitmap_range": (_I, [_P, _I, _U64, _U64, _U64, _P, _U64, _P]),
     "rlk_fusion_merge": (_I, [C.POINTER(FusionPlanC), _I, _I, _I, _I, _P, _P, _I, _P, _U64, _D, _P, _U64, _I,
-                              _P, _P]),
+                              _P, _I, _P]),
     "rlk_grpo_fwd": (_I, [_P, _I, _U64, _U64, _U64, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.POINTER(ClipC), _P, _P,
                           _P, _P, _P, _P, _U64, _P]),
     "rlk_segment_sum_f64": (_I, [_P, _P, _U64, _P, _P]),

@@ -172,15 +172,37 @@ def save(path, tensors: Mapping[str, object]) -> None:
         e.checksum = _u64(checksum_device(devs[e.name]))
     path = Path(path)
     tmp = path.with_name(path.name + ".tmp")
-    with open(tmp, "wb") as f:
-        f.write(encode_header(entries))
-        for e in entries:
-            t = devs[e.name].contiguous()
-            raw = (t.view(torch.int16) if t.dtype == torch.bfloat16 else t).cpu().numpy().tobytes()
-            f.seek(e.offset)
-            f.write(raw)
-        f.truncate(size)
-    os.replace(tmp, path)
+    try:
+        with open(tmp, "wb") as f:
+            f.write(encode_header(entries))
+            for e in entries:
+                t = devs[e.name].contiguous()
+                raw = (t.view(torch.int16) if t.dtype == torch.bfloat16 else t).cpu().numpy().tobytes()
+                f.seek(e.offset)
+                f.write(raw)
+            f.truncate(size)
+            f.flush()
+            os.fsync(f.fileno())
+        os.replace(tmp, path)
+    except BaseException:
+        if tmp.exists():
+            tmp.unlink()
+        raise
+    _fsync_dir(path)
+
+
+def _fsync_dir(path: Path) -> None:
+    """Persist a rename: fsync the directory entry (best effort on filesystems without dir fds)."""
+    try:
+        fd = os.open(path.parent, os.O_RDONLY)
+    except OSError:
+        return
+    try:
+        os.fsync(fd)
+    except OSError:
+        pass
+    finally:
+        os.close(fd)
 
 
 def open_mmap(path) -> tuple[list[Entry], dict[str, np.memmap]]:
@@ -244,11 +266,16 @@ class FuseReport:
     h2d_bytes: int
     d2h_bytes: int
     groups: int
+    passthrough: list = None  # tensors no expert changed (written as the base; see fuse_streaming)
 
 
 def cmd_fuse(base_path, expert_paths: Sequence, out_path, cfg: FusionConfig = FusionConfig(),
-             device_budget_bytes: int = 32 << 30) -> FuseReport:
-    """Fuse checkpoint files: fused checkpoint + per-tensor FusionStats report."""
+             device_budget_bytes: int = 32 << 30, on_unchanged: str = "passthrough") -> FuseReport:
+    """Fuse checkpoint files: fused checkpoint + per-tensor FusionStats report.
+
+    Validation happens before the output is renamed into place: non-finite inputs raise
+    ValueError("logits must be finite"); tensors no expert changed are written as the base and listed
+    in `report.passthrough` (on_unchanged="raise": the reference's mean-norm ValueError instead)."""
     from .loader import ArraySource, HostLoader, fuse_streaming
     if not expert_paths:
         raise ValueError("need at least one task vector")
@@ -274,18 +301,23 @@ def cmd_fuse(base_path, expert_paths: Sequence, out_path, cfg: FusionConfig = Fu
         ld = HostLoader()
         try:
             rep = fuse_streaming(names, [e.numel for e in base_e], len(experts), ArraySource(base_m, [m for _, m in experts]),
-                                 sink, cfg, dtype=dt, device_budget_bytes=device_budget_bytes, loader=ld)
+                                 sink, cfg, dtype=dt, device_budget_bytes=device_budget_bytes, loader=ld,
+                                 on_unchanged=on_unchanged)
         finally:
             ld.close()
         for m in out_maps.values():
             m.flush()
+        del out_maps
         for e in entries:
             e.checksum = _u64(sink.sums[e.name])
         with open(tmp, "r+b") as f:
             f.write(encode_header(entries))
+            f.flush()
+            os.fsync(f.fileno())
         os.replace(tmp, out_path)
     except BaseException:
         if tmp.exists():
             tmp.unlink()
         raise
-    return FuseReport(rep.stats, rep.h2d_bytes, rep.d2h_bytes, rep.groups)
+    _fsync_dir(out_path)
+    return FuseReport(rep.stats, rep.h2d_bytes, rep.d2h_bytes, rep.groups, rep.passthrough)

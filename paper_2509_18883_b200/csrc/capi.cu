@@ -61,7 +61,7 @@ extern "C" {
 
 const char* rlk_last_error(void) { return g_last_error; }
 
-int rlk_abi_version(void) { return 1; }
+int rlk_abi_version(void) { return 2; }  // 2: rlk_fusion_merge takes exact_path
 
 int rlk_device_sm_count(int device) {
   int n = 0;

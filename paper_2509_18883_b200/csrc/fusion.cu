@@ -1285,7 +1285,7 @@ int rlk_fusion_mask_bitmap(const uint64_t* child_seeds, int n_experts, uint64_t 
 int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, int dtype_out, int delta_mode,
                      const double* scale, const double* weights, int dropout_mode, const uint64_t* child_seeds,
                      uint64_t thresh, double keep_prob, const uint32_t* bitmap, uint64_t words_per_row,
-                     int erase_mode, unsigned long long* counters, void* stream) {
+                     int erase_mode, unsigned long long* counters, int exact_path, void* stream) {
   RLK_REQUIRE(plan && scale && weights && counters, "rlk_fusion_merge: NULL argument");
   RLK_REQUIRE(n_experts >= 1 && n_experts <= RLK_MAX_EXPERTS, "rlk_fusion_merge: bad expert count %d", n_experts);
   RLK_REQUIRE(dropout_mode >= 0 && dropout_mode <= 2, "rlk_fusion_merge: bad dropout mode %d", dropout_mode);
@@ -1313,8 +1313,7 @@ int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, i
   a.erase_mode = erase_mode;
   a.delta_mode = delta_mode & 1;
   a.with_base = (delta_mode & 1) ? ((delta_mode >> 1) & 1) : 1;
-  const char* env = getenv("RLK_MERGE_FAST");
-  a.fast = env ? atoi(env) : 1;
+  a.fast = exact_path ? 0 : 1;
   cudaStream_t s = (cudaStream_t)stream;
   switch (dtype_in) {
     case RLK_BF16: return dispatch_merge_out<RLK_BF16>(dtype_out, n_experts, a, s);

@@ -20,7 +20,6 @@ tensor that no expert changed passes through as the base instead of raising the 
 from __future__ import annotations
 
 import math
-import os
 from dataclasses import dataclass
 from typing import Literal, Mapping, Sequence, Union
 
@@ -248,7 +247,7 @@ class FusionCall:
 
     def __init__(self, pieces: Sequence[Piece], layout: FusionLayout, n_experts: int, cfg: FusionConfig,
                  *, delta_mode: bool = False, with_base: bool = True, group=None, stream=None,
-                 dropout_mode: int | None = None, async_upload: bool = True):
+                 dropout_mode: int | None = None, async_upload: bool = True, exact_merge: bool = False):
         if not 1 <= n_experts <= L.RLK_MAX_EXPERTS:
             raise NotImplementedError(f"the B200 kernels fuse 1..{L.RLK_MAX_EXPERTS} experts, got {n_experts}")
         if not pieces:
@@ -275,9 +274,10 @@ class FusionCall:
         self.status = torch.empty(nt, dtype=torch.int32, device=self.device)
         self.counters = torch.zeros((nt, 2 * n_experts), dtype=torch.int64, device=self.device)
         self.partials = None
+        # exact_merge: K3 runs the reference-order f64 kernel instead of the certified f32x2 fast path
+        # (same results; the parity tests compare the two)
+        self.exact_merge = exact_merge
         p = cfg.dropout_p
-        if dropout_mode is None:  # RLK_DROPOUT_MODE=1/2: test hook forcing inline / bitmap keep bits
-            dropout_mode = int(os.environ.get("RLK_DROPOUT_MODE", "-1"))
         if p == 0.0:
             dropout_mode = 0
         elif dropout_mode not in (1, 2):
@@ -412,7 +412,7 @@ class FusionCall:
             self._launch("rlk_fusion_merge", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
                    L.dtype_code(dto), dmode, L.ptr(self.scale), w, self.dropout_mode,
                    seeds if self.dropout_mode else None, self.thresh, self.keep_prob,
-                   L.ptr(self.bitmap), self.words_per_row, erase, L.ptr(self.counters), s)
+                   L.ptr(self.bitmap), self.words_per_row, erase, L.ptr(self.counters), int(self.exact_merge), s)
         return self
 
     def stats(self, tensor: int, weights: Sequence[float], size: int | None = None,
@@ -619,7 +619,7 @@ def erase_minority(taus: Sequence[TaskVector], weighting: str = "sum") -> list[T
 
 # ----------------------------------------------------------------------------- fuse / merge
 def fuse(theta_sft: ParamTable, taus: Sequence[TaskVector], cfg: FusionConfig,
-         out_dtype: torch.dtype | None = None) -> tuple[ParamTable, FusionStats]:
+         out_dtype: torch.dtype | None = None, *, exact_merge: bool = False) -> tuple[ParamTable, FusionStats]:
     """normalize -> dropout -> erase -> weighted sum, with FusionStats (fusion.py:154-188).
 
     One K1 + finalize + K3 pass over (base, experts); the output keeps the base's dtype unless
@@ -651,7 +651,8 @@ def fuse(theta_sft: ParamTable, taus: Sequence[TaskVector], cfg: FusionConfig,
     dto = out_dtype or base.dtype
     out = torch.empty(base.shape, dtype=dto, device=base.device)
     piece = Piece(0, 0, _flat(b), [_flat(e) for e in experts], out.view(-1))
-    call = FusionCall([piece], FusionLayout([piece.numel]), len(taus), cfg, delta_mode=not pair)
+    call = FusionCall([piece], FusionLayout([piece.numel]), len(taus), cfg, delta_mode=not pair,
+                      exact_merge=exact_merge)
     call.norms()
     call.check_status()
     call.merge(weights, dtype_out=dto)
@@ -687,12 +688,14 @@ class FusionReport:
 def fuse_state_dict(base: Mapping[str, torch.Tensor], experts: Sequence[Mapping[str, torch.Tensor]],
                     cfg: FusionConfig = FusionConfig(), *, out_dtype: torch.dtype | None = None,
                     out: Mapping[str, torch.Tensor] | None = None, stream=None,
-                    check: bool = True) -> tuple[dict[str, torch.Tensor], FusionReport]:
+                    check: bool = True, exact_merge: bool = False,
+                    dropout_mode: int | None = None) -> tuple[dict[str, torch.Tensor], FusionReport]:
     """Fuse whole checkpoints: per tensor the reference `fuse` with one shared cfg, in ONE K1 launch,
     one finalize and ONE K3 launch over every tensor (plus K2 when dropout_p > 0).
 
     All tensors must be CUDA tensors of one dtype (bf16 / f32 / f64).  `check` synchronises once at
-    the end and raises ValueError on non-finite inputs."""
+    the end and raises ValueError on non-finite inputs.  `exact_merge` / `dropout_mode` (1 inline keep
+    bits, 2 K2 bitmap) pin the kernel variants; every choice gives the same results."""
     names = list(base.keys())
     n = len(experts)
     if n == 0:
@@ -716,7 +719,7 @@ def fuse_state_dict(base: Mapping[str, torch.Tensor], experts: Sequence[Mapping[
         outs[name] = o
         pieces.append(Piece(k, 0, _flat(b), [_flat(e) for e in es], o.view(-1)))
     layout = FusionLayout([p.numel for p in pieces])
-    call = FusionCall(pieces, layout, n, cfg, stream=stream)
+    call = FusionCall(pieces, layout, n, cfg, stream=stream, exact_merge=exact_merge, dropout_mode=dropout_mode)
     call.norms()
     call.merge(weights, dtype_out=dto)
     if check:

@@ -137,6 +137,7 @@ class StreamingReport:
     groups: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    passthrough: list = field(default_factory=list)  # tensors no expert changed (written as the base)
 
 
 def plan_groups(numels: Sequence[int], n_experts: int, esize: int, budget_bytes: int) -> list[list[int]]:
@@ -182,7 +183,8 @@ def _footprint(n: int, n_experts: int, esize: int) -> int:
 def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, source, sink,
                    cfg: FusionConfig = FusionConfig(), dtype: torch.dtype = torch.bfloat16,
                    device_budget_bytes: int = 64 << 30, stats: bool = True,
-                   loader: HostLoader | None = None, group_bytes: int = 2 << 30) -> StreamingReport:
+                   loader: HostLoader | None = None, group_bytes: int = 2 << 30,
+                   on_unchanged: str = "passthrough") -> StreamingReport:
     """Fuse a host-resident (or synthesised) checkpoint through the device in pipelined groups.
 
     Consecutive tensors are grouped up to min(`group_bytes`, half the budget) of device footprint
@@ -192,7 +194,13 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
     the host) for the D2H of every earlier group whose ring space it reuses.  Pinned host
     sources/sinks are DMA'd directly; pageable ones go through the loader's pinned slots.  Blocking
     sinks (pageable outputs, checksums) run on a worker thread with their own loader, overlapping the
-    main thread's H2D staging."""
+    main thread's H2D staging.
+
+    After the last group: non-finite inputs raise ValueError("logits must be finite"); tensors no
+    expert changed are listed in `report.passthrough` (written as the base), or raise the reference's
+    "cannot take mean norm of all-zero task vectors" with on_unchanged="raise"."""
+    if on_unchanged not in ("passthrough", "raise"):
+        raise ValueError("on_unchanged must be 'passthrough' or 'raise'")
     dev = torch.device("cuda", torch.cuda.current_device())
     esize = torch.tensor([], dtype=dtype).element_size()
     cap = device_budget_bytes // esize // 64 * 64  # ring capacity in elements
@@ -276,6 +284,22 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
         for f in freed.values():
             f.result()  # re-raises a sink error
         torch.cuda.synchronize(dev)
+        # finalize's per-tensor status (fusion.cu k_finalize): 2 = non-finite input (the reference's
+        # ParamTable rejects it, toy_env.py:71-72), 1 = no expert changed the tensor (the reference's
+        # per-tensor fuse raises, fusion.py:97-98; the state-dict path writes the base unchanged)
+        bad, unchanged = [], []
+        for group, _, call in plans:
+            for t, st in zip(group, call.status.cpu().tolist()):
+                if st == 2:
+                    bad.append(names[t])
+                elif st == 1:
+                    unchanged.append(names[t])
+        if bad:
+            raise ValueError(f"logits must be finite (non-finite values in {bad[:8]}"
+                             f"{' ...' if len(bad) > 8 else ''})")
+        if unchanged and on_unchanged == "raise":
+            raise ValueError("cannot take mean norm of all-zero task vectors")
+        rep.passthrough = unchanged
         if stats:
             for group, _, call in plans:
                 host = call.host_tables()

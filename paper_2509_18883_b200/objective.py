@@ -288,20 +288,56 @@ def grpo_forward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = Clip
     return GRPOForward(tot[0] / batch.n_groups, gs, logp, lse, term, coef, flags)
 
 
+def _row_csr(row_index: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Tokens grouped by the logits row they read: (distinct rows ascending, CSR pointers, token ids in
+    stable order) -- tokens sharing a row accumulate in the reference's order (objective.py:278-282)."""
+    order = torch.sort(row_index, stable=True).indices
+    rows, counts = torch.unique_consecutive(row_index[order], return_counts=True)
+    ptr = torch.zeros(rows.numel() + 1, dtype=torch.int64, device=row_index.device)
+    torch.cumsum(counts, 0, out=ptr[1:])
+    return rows.contiguous(), ptr, order.contiguous()
+
+
 def grpo_backward(logits: torch.Tensor, batch: GRPOBatch, fwd: GRPOForward, grad_scale: torch.Tensor | float = 1.0,
                   grad_dtype: torch.dtype | None = None, *, stream=None) -> torch.Tensor:
-    """K5: dJ/dlogits for one-row-per-token batches, scaled by `grad_scale` (the autograd grad_out)."""
+    """K5: grad_scale * dJ/dlogits, same shape as `logits` (the autograd grad_out is `grad_scale`).
+
+    Without `row_index`, token r reads logits row r (the batch's rows must not exceed the logits'; rows
+    past the batch get a zero gradient).  With `row_index`, every distinct row read is written once as
+    the sum over the tokens that read it (CSR), and rows no token reads are zero (objective.py:253-283)."""
     if stream is not None:
         with torch.cuda.stream(stream):
             return grpo_backward(logits, batch, fwd, grad_scale, grad_dtype)
+    if logits.ndim != 2:
+        raise ValueError("logits must be [rows, vocab]")
+    logits = logits.contiguous()
     R, V = logits.shape
+    nb = batch.n_rows
     coef = fwd.coef if (isinstance(grad_scale, float) and grad_scale == 1.0) else fwd.coef * grad_scale
     coef = coef.contiguous()
     temp_tok = batch.temperature[batch.sample_of_row.long()].contiguous()
-    grad = torch.empty((R, V), dtype=grad_dtype or logits.dtype, device=logits.device)
-    L.call("rlk_grpo_bwd", L.ptr(logits), L.dtype_code(logits.dtype), R, V, V, L.ptr(batch.row_index), None, None,
-           L.ptr(batch.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(coef), L.ptr(grad),
-           L.dtype_code(grad.dtype), V, L.stream_handle(stream))
+    gdt = grad_dtype or logits.dtype
+    s = L.stream_handle(stream)
+    if batch.row_index is None:
+        if nb > R:
+            raise ValueError(f"batch has {nb} token rows but logits only {R}")
+        grad = torch.empty((R, V), dtype=gdt, device=logits.device)
+        if nb < R:
+            grad[nb:].zero_()
+        L.call("rlk_grpo_bwd", L.ptr(logits), L.dtype_code(logits.dtype), nb, V, V, None, None, None,
+               L.ptr(batch.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(coef), L.ptr(grad),
+               L.dtype_code(grad.dtype), V, s)
+        return grad
+    ri = batch.row_index
+    if nb and (int(ri.min()) < 0 or int(ri.max()) >= R):
+        raise IndexError(f"row_index out of range [0, {R})")
+    grad = torch.zeros((R, V), dtype=gdt, device=logits.device)
+    if nb == 0:
+        return grad
+    rows, ptr_, order = _row_csr(ri)
+    L.call("rlk_grpo_bwd", L.ptr(logits), L.dtype_code(logits.dtype), rows.numel(), V, V, L.ptr(rows), L.ptr(ptr_),
+           L.ptr(order), L.ptr(batch.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(coef), L.ptr(grad),
+           L.dtype_code(grad.dtype), V, s)
     return grad
 
 
@@ -438,7 +474,12 @@ def _pack_masked_batch(batch: MaskedBatch, params: ParamTable) -> tuple[GRPOBatc
                     raise IndexError(f"index {tok} is out of bounds for axis 0 with size {V}")
                 toks.append(tok % V)  # numpy indexing wraps negative ids (objective.py:244)
                 rows.append(sample.context_id * T + t)
-            lt.extend(float(x) for x in sample.train_logps)
+            # the reference reads train_logps[t] for t < len(tokens) only (objective.py:243-247): extra
+            # entries are ignored, a short list raises IndexError at the first missing position
+            n_tok = len(sample.tokens)
+            if len(sample.train_logps) < n_tok:
+                raise IndexError("tuple index out of range")
+            lt.extend(float(x) for x in sample.train_logps[:n_tok])
             li.extend(float(x) for x in sample.infer_logps)
             cu.append(len(toks))
             adv.append(float(a))
@@ -496,22 +537,8 @@ def objective_gradient(batch: MaskedBatch, params: ParamTable, clip: ClipConfig)
         return grad
     logits2d = params.logits.reshape(-1, params.vocab_size)
     fwd = grpo_forward(logits2d, b, clip)
-    rows_np = np.asarray(rows, dtype=np.int64)
-    order = np.argsort(rows_np, kind="stable")
-    uniq, starts = np.unique(rows_np[order], return_index=True)
-    ptr = np.append(starts, len(order)).astype(np.int64)
-    dev = grad.device
-    temp_tok = b.temperature[b.sample_of_row.long()].contiguous()
-    g2d = grad.view(-1, params.vocab_size)
-    V = params.vocab_size
-    # keep every device argument referenced until the launch is enqueued (no freed temporaries)
-    urows = torch.from_numpy(uniq).to(dev)
-    row_ptr = torch.from_numpy(ptr).to(dev)
-    row_tok = torch.from_numpy(order.astype(np.int64)).to(dev)
-    L.call("rlk_grpo_bwd", L.ptr(logits2d), L.dtype_code(logits2d.dtype), len(uniq), V, V, L.ptr(urows),
-           L.ptr(row_ptr), L.ptr(row_tok), L.ptr(b.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(fwd.coef),
-           L.ptr(g2d), L.RLK_F64, V, L.stream_handle())
-    return grad
+    # K5 over the distinct (context, position) rows; tokens sharing a row accumulate (CSR)
+    return grpo_backward(logits2d, b, fwd, grad_dtype=torch.float64).view(params.shape)
 
 
 def ascent_step(params: ParamTable, gradient, lr: float) -> ParamTable:

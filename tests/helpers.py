@@ -48,3 +48,44 @@ def synth_state_dicts(shapes, n_experts=3, seed=0, dtype_round=None):
             e = b + g.normal(0.0, (i + 1) * 1e-3, shp)
             experts[i][name] = dtype_round(e) if dtype_round else e
     return base, experts
+
+
+def grad_rows_error(got, z, tokens, coef, temps, rtol, floor=1e-30):
+    """Per-element parity of gradient rows with the reference (objective.py:271-282).
+
+    got[k] is the kernel's row for token k (logits z[k], f64), coef[k] the kernel's own dJ/dlogit scale.
+    The reference row is coef * (onehot(token) - softmax(z / T)) in float64; every entry must satisfy
+    |got - ref| <= rtol * |coef| * (p + onehot) + floor, i.e. a RELATIVE bound on each softmax entry
+    (entries down to ~1e-11 of the row are checked, not only the few above an absolute tolerance).
+    Returns (max of |got - ref| / bound, index of that entry); the row passes iff the max <= 1."""
+    worst, where = 0.0, None
+    for k in range(len(tokens)):
+        zz = np.asarray(z[k], dtype=np.float64) / temps[k]
+        m = zz.max()
+        e = np.exp(zz - m)
+        p = e / e.sum()
+        ref = -coef[k] * p
+        ref[int(tokens[k])] += coef[k]
+        onehot = np.zeros_like(p)
+        onehot[int(tokens[k])] = 1.0
+        bound = rtol * abs(coef[k]) * (p + onehot) + floor
+        r = np.abs(np.asarray(got[k], dtype=np.float64) - ref) / bound
+        j = int(np.argmax(r))
+        if r[j] > worst:
+            worst, where = float(r[j]), (k, j)
+    return worst, where
+
+
+def assert_grad_rows(got, z, tokens, coef, temps, rtol, floor=1e-30):
+    worst, where = grad_rows_error(got, z, tokens, coef, temps, rtol, floor)
+    assert worst <= 1.0, f"gradient entry {where} off by {worst:.3g}x the per-element bound (rtol {rtol})"
+    # the check has teeth: the same rows with every non-target entry zeroed must fail it
+    bad = np.array(got, dtype=np.float64, copy=True)
+    for k in range(len(tokens)):
+        if coef[k] != 0.0:
+            keep = bad[k][int(tokens[k])]
+            bad[k][:] = 0.0
+            bad[k][int(tokens[k])] = keep
+    if any(c != 0.0 for c in coef):
+        assert grad_rows_error(bad, z, tokens, coef, temps, rtol, floor)[0] > 1.0
+    return worst

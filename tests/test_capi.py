@@ -31,7 +31,7 @@ def test_library_exports_all_declared_symbols():
     handle = ctypes.CDLL(str(_lib.LIB_PATH))
     missing = [s for s in declared_symbols() if not hasattr(handle, s)]
     assert not missing, missing
-    assert handle.rlk_abi_version() == 1
+    assert handle.rlk_abi_version() == 2
     # every declared symbol has a ctypes signature in the binding
     assert not [s for s in declared_symbols() if s not in _lib.SIGNATURES]
 
@@ -57,9 +57,9 @@ def test_more_argument_checks_before_any_device_work():
     plan = ctypes.byref(L.FusionPlanC(8, 8, 1, 1))
     w = (ctypes.c_double * 3)(1 / 3, 1 / 3, 1 / 3)
     with pytest.raises(ValueError, match="bad erase mode"):
-        L.call("rlk_fusion_merge", plan, 3, 0, 0, 0, 8, w, 0, None, 0, 1.0, None, 0, 5, 8, None)
+        L.call("rlk_fusion_merge", plan, 3, 0, 0, 0, 8, w, 0, None, 0, 1.0, None, 0, 5, 8, 0, None)
     with pytest.raises(ValueError, match="bad dropout mode"):
-        L.call("rlk_fusion_merge", plan, 3, 0, 0, 0, 8, w, 7, seeds, 0, 1.0, None, 0, 1, 8, None)
+        L.call("rlk_fusion_merge", plan, 3, 0, 0, 0, 8, w, 7, seeds, 0, 1.0, None, 0, 1, 8, 0, None)
     clip = L.ClipC(0.2, 0.2, 3.0, 2.0, 1)
     with pytest.raises(ValueError, match="bad dtype"):
         L.call("rlk_grpo_fwd", 8, 9, 4, 16, 16, None, 8, 8, 8, 8, 8, 8, 8, 8, ctypes.byref(clip), None, None, 8, 8, 8,

@@ -12,7 +12,7 @@ import pytest
 import torch
 
 from oracle import fusion as OF
-from tests.helpers import rne_bf16_bits
+from tests.helpers import assert_grad_rows, rne_bf16_bits
 
 pytestmark = pytest.mark.gpu
 
@@ -54,13 +54,16 @@ def config3(cuda):
     torch.cuda.empty_cache()
 
 
-def test_fullsize_fast_equals_reference_order(config3, monkeypatch):
+def test_fullsize_fast_equals_reference_order(config3):
     names, pieces, call = config3
     fast = _checksums([p.out for p in pieces])
     counters = call.counters.clone()
-    monkeypatch.setenv("RLK_MERGE_FAST", "0")
     call.counters[:, 3:].zero_()  # the erased counts are K3's; the non-zero counts stay from K1
-    call.merge((1 / 3,) * 3)
+    call.exact_merge = True
+    try:
+        call.merge((1 / 3,) * 3)
+    finally:
+        call.exact_merge = False
     torch.cuda.synchronize()
     exact = _checksums([p.out for p in pieces])
     assert torch.equal(fast, exact)
@@ -129,10 +132,12 @@ def test_fullsize_grpo_config5_chunk(cuda):
     np.testing.assert_allclose(fwd.logp.cpu().numpy()[rows], logp, rtol=0, atol=2e-6)
     np.testing.assert_allclose(fwd.term.cpu().numpy()[rows], term, rtol=1e-5, atol=1e-15)
     np.testing.assert_allclose(fwd.coef.cpu().numpy()[rows], coef, rtol=1e-5, atol=1e-18)
-    gref = OO.gradient_rows(z, None, toks[rows], coef, [0.7] * len(rows), z.shape)
-    gg = grad[torch.from_numpy(rows).to(cuda)].float().double().cpu().numpy()
-    scale = np.abs(coef).max()
-    np.testing.assert_allclose(gg, gref, rtol=0, atol=1e-2 * scale + 1e-15)
+    # every entry of the sampled bf16 gradient rows (131,072 each) vs coef * (onehot - softmax) in f64,
+    # relative per element (bf16 unit roundoff 2^-8 + the f32 row arithmetic)
+    gg = grad[torch.from_numpy(rows).to(cuda)].double().cpu().numpy()
+    cf = fused.coef.cpu().numpy()[rows]
+    worst = assert_grad_rows(gg, z, toks[rows], cf, [0.7] * len(rows), 2.0 ** -8 + 1e-5)
+    print(f"config-5 chunk: worst per-element gradient error = {worst:.3f} of the bound")
     sums = grad.float().sum(dim=1).double().cpu().numpy()
     cmax = np.abs(fused.coef.cpu().numpy())
     assert np.all(np.abs(sums) <= 1e-2 * cmax + 1e-12)

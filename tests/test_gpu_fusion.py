@@ -26,11 +26,11 @@ def _pt(x, dtype, dev):
     return ParamTable(torch.from_numpy(np.asarray(x, dtype=np.float64).reshape(1, 1, -1)).to(dev, dtype))
 
 
-def _fuse(base, experts, cfgkw, dtype, dev, out_dtype=None):
+def _fuse(base, experts, cfgkw, dtype, dev, out_dtype=None, exact_merge=False):
     from paper_2509_18883_b200 import fusion as F
     b = _pt(base, dtype, dev)
     taus = [F.task_vector(_pt(e, dtype, dev), b) for e in experts]
-    return F.fuse(b, taus, F.FusionConfig(**cfgkw), out_dtype=out_dtype)
+    return F.fuse(b, taus, F.FusionConfig(**cfgkw), out_dtype=out_dtype, exact_merge=exact_merge)
 
 
 @pytest.mark.parametrize("cname", list(CFGS))
@@ -49,14 +49,13 @@ def test_fuse_kat_f64(cuda, golden_fusion, cname):
     assert (got == base).sum() == (ref == base).sum()
 
 
-@pytest.mark.parametrize("fast", ["1", "0"])
+@pytest.mark.parametrize("exact", [False, True])
 @pytest.mark.parametrize("cname", ["default", "p05_s42", "p05_s42_sq", "p03_s7_t1_w", "p09_s3_none", "none_noerase"])
-def test_fuse_bf16_exact(cuda, golden_fusion, cname, fast, monkeypatch):
-    """bf16 in / bf16 out must equal RNE_bf16(reference f64 output) bit for bit."""
-    monkeypatch.setenv("RLK_MERGE_FAST", fast)
+def test_fuse_bf16_exact(cuda, golden_fusion, cname, exact):
+    """bf16 in / bf16 out must equal RNE_bf16(reference f64 output) bit for bit (fast and exact K3)."""
     base = golden_fusion["bf16/base"]
     experts = [golden_fusion[f"bf16/expert{k}"] for k in range(3)]
-    fused, st = _fuse(base, experts, CFGS[cname], torch.bfloat16, cuda)
+    fused, st = _fuse(base, experts, CFGS[cname], torch.bfloat16, cuda, exact_merge=exact)
     got = fused.logits.reshape(-1).view(torch.int16).cpu().numpy().view(np.uint16)
     ref = rne_bf16_bits(golden_fusion[f"bf16/{cname}/fused"])
     mism = np.flatnonzero(got != ref)
@@ -162,13 +161,9 @@ def test_dropout_bitmap_equals_inline(cuda):
     to = lambda d: {k: torch.from_numpy(v).to(cuda, torch.bfloat16) for k, v in d.items()}
     cfg = F.FusionConfig(dropout_p=0.5, seed=9)
     res = []
-    for mode in ("1", "2"):
-        os.environ["RLK_DROPOUT_MODE"] = mode
-        try:
-            outs, rep = F.fuse_state_dict(to(base), [to(e) for e in experts], cfg)
-        finally:
-            del os.environ["RLK_DROPOUT_MODE"]
-        assert rep.call.dropout_mode == int(mode)
+    for mode in (1, 2):
+        outs, rep = F.fuse_state_dict(to(base), [to(e) for e in experts], cfg, dropout_mode=mode)
+        assert rep.call.dropout_mode == mode
         res.append((outs, rep.call.counters.cpu()))
     for k in res[0][0]:
         assert torch.equal(res[0][0][k], res[1][0][k])
@@ -218,9 +213,8 @@ def test_fast_path_equals_exact_path_random(cuda, monkeypatch):
     for cfg in (F.FusionConfig(), F.FusionConfig(dropout_p=0.5, seed=1), F.FusionConfig(erase_weighting="squared"),
                 F.FusionConfig(target_norm=None)):
         outs = []
-        for fast in ("1", "0"):
-            monkeypatch.setenv("RLK_MERGE_FAST", fast)
-            o, rep = F.fuse_state_dict({"w": base}, [{"w": e} for e in experts], cfg)
+        for exact in (False, True):
+            o, rep = F.fuse_state_dict({"w": base}, [{"w": e} for e in experts], cfg, exact_merge=exact)
             outs.append((o["w"], rep.call.counters.clone()))
         assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16)), cfg
         assert torch.equal(outs[0][1], outs[1][1]), cfg
@@ -338,9 +332,9 @@ def test_fast_path_adversarial_values(cuda, monkeypatch):
     for cfgkw in (dict(dropout_p=0.5, seed=4), dict(target_norm=None, dropout_p=0.5, seed=4),
                   dict(erase_weighting="squared", merge_weights=(0.5, 0.3, 0.2))):
         outs = []
-        for fast in ("1", "0"):
-            monkeypatch.setenv("RLK_MERGE_FAST", fast)
-            o, rep = F.fuse_state_dict({"w": bt}, [{"w": e} for e in ets], F.FusionConfig(**cfgkw))
+        for exact in (False, True):
+            o, rep = F.fuse_state_dict({"w": bt}, [{"w": e} for e in ets], F.FusionConfig(**cfgkw),
+                                       exact_merge=exact)
             outs.append((o["w"].clone(), rep.call.counters.clone()))
         assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16)), cfgkw
         assert torch.equal(outs[0][1], outs[1][1]), cfgkw

@@ -94,3 +94,38 @@ def test_loader_roundtrip_and_checksum(cuda):
     s.synchronize()
     assert torch.equal(a, b) and 0.015 < float(a.float().std()) < 0.025
     ld.close()
+
+
+def test_streaming_validates_inputs(cuda, tmp_path):
+    """fuse_streaming / cmd_fuse check finalize's per-tensor status after the last group: a non-finite
+    input raises the reference's ValueError (and cmd_fuse leaves no output file); a tensor no expert
+    changed is written as the base and reported (or raises the reference's mean-norm error on request)."""
+    from paper_2509_18883_b200 import checkpoint as CK
+    from paper_2509_18883_b200 import fusion as F
+    from paper_2509_18883_b200.loader import ArraySink, ArraySource, fuse_streaming
+    shapes = {"a": (64, 33), "same": (100,), "c": (50, 7)}
+    base, experts = synth_state_dicts(shapes, 3, seed=5, dtype_round=bf16_round)
+    for e in experts:
+        e["same"] = base["same"].copy()
+    hb, he = _host_bf16(base), [_host_bf16(e) for e in experts]
+    names = list(hb)
+    numels = [hb[k].numel() for k in names]
+    out = {k: torch.empty(v.shape, dtype=torch.bfloat16) for k, v in hb.items()}
+    rep = fuse_streaming(names, numels, 3, ArraySource(hb, he), ArraySink(out), F.FusionConfig())
+    assert rep.passthrough == ["same"]
+    assert torch.equal(out["same"].view(torch.int16), hb["same"].view(torch.int16))
+    with pytest.raises(ValueError, match="cannot take mean norm of all-zero task vectors"):
+        fuse_streaming(names, numels, 3, ArraySource(hb, he), ArraySink(out), F.FusionConfig(), on_unchanged="raise")
+    he[1]["c"][3, 4] = float("nan")
+    with pytest.raises(ValueError, match="logits must be finite"):
+        fuse_streaming(names, numels, 3, ArraySource(hb, he), ArraySink(out), F.FusionConfig())
+    # cmd_fuse: same checks before the rename, so no partial output exists
+    paths = []
+    for i, d in enumerate([hb] + he):
+        p = tmp_path / f"in{i}.rlk"
+        CK.save(p, d)
+        paths.append(p)
+    dst = tmp_path / "fused.rlk"
+    with pytest.raises(ValueError, match="logits must be finite"):
+        CK.cmd_fuse(paths[0], paths[1:], dst, F.FusionConfig())
+    assert not dst.exists() and not (tmp_path / "fused.rlk.tmp").exists()
