@@ -104,10 +104,10 @@ def test_tensor_api_vs_oracle(cuda, dtype, tau):
     assert flip.sum() <= 1
     np.testing.assert_allclose(cg[~flip], coef[~flip], rtol=1e-5, atol=0)
     # backward, EVERY entry of every row vs coef * (onehot - softmax) in f64 (per-element relative bound):
-    # f32 grad: ex2.approx + f32 argument rounding + the f32 row log-sum-exp -> rtol 1e-5;
+    # f32 grad: ex2.approx + f32 argument rounding + the f32 row log-sum-exp -> rtol 5e-6 (measured <= 2.3e-6);
     # bf16 grad: plus one bf16 rounding (unit roundoff 2^-8)
     temps = [tau] * len(toks)
-    for gdt, rtol in ((torch.float32, 1e-5), (torch.bfloat16, 2.0 ** -8 + 1e-5)):
+    for gdt, rtol in ((torch.float32, 5e-6), (torch.bfloat16, 2.0 ** -8 + 5e-6)):
         grad = O.grpo_backward(lg, b, fwd, grad_dtype=gdt).double().cpu().numpy()
         worst = assert_grad_rows(grad, logits, toks, cg, temps, rtol)
         print(f"grad {gdt} {dtype} tau={tau}: worst per-element error = {worst:.3f} of the bound")
