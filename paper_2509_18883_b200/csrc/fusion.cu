@@ -778,11 +778,13 @@ __device__ __forceinline__ float sign_one(float x) {
   asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(r) : "r"(__float_as_uint(x)), "r"(0x80000000u), "r"(0x3f800000u));
   return __uint_as_float(r);
 }
-// the bf16 rounding midpoint of the interval containing y: (bits & 0xffff0000) | 0x8000 (one LOP3)
-__device__ __forceinline__ float mid_of(float y) {
-  uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(r) : "r"(__float_as_uint(y)), "r"(0xffff0000u), "r"(0x8000u));
-  return __uint_as_float(r);
+// (x, y) rounded to nearest-even bf16, packed lo | hi << 16 (one F2FP)
+__device__ __forceinline__ uint32_t pack_bf16x2(float2 v) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(v.x, v.y);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+__device__ __forceinline__ float fmin4_nan(float a, float b, float c, float d) {
+  return fmin_nan(fmin3_nan(a, b, c), d);
 }
 
 // Fast K3 for bf16 experts + bf16 base -> bf16 (the checkpoint path): f32x2 arithmetic with certified
@@ -843,6 +845,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
     return;
   }
   const int tid = threadIdx.x;
+  // 4 elements per thread: the thread's keep bits are the low (even tid) or high (odd tid) nibble of a
+  // bitmap byte, every iteration (le & 4 == (tid & 1) * 4 since kFastCThreads is even).  Multiplying
+  // the masked nibble moves bit k to bit 8k + 7 (distinct partial products, no carries).
+  const uint32_t nib_mask = (tid & 1) ? 0xf0u : 0x0fu;
+  const uint32_t nib_mul = (tid & 1) ? 0x01020408u : 0x10204080u;
   const float cv = ERASE == 1 ? 0x1p-20f : 0x1p-19f;
   float w32[N], wh32[N];
   float wmax = 0.f;
@@ -893,21 +900,27 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           xw4[i] = FastVec::load(sb + (i + 1) * SB + v * (2 * kFastElems));
-          kb[i] = DROP ? ((uint32_t)bm[i * BMB + (le >> 3)] >> (le & 7)) : 0xffu;
+          kb[i] = DROP ? (uint32_t)bm[i * BMB + (le >> 3)] : 0xffu;
         }
-        // dropout on the integer side: the thread's 4 keep bits go to byte sign bits (one IMAD), PRMT
-        // sign-replication turns them into halfword masks, and one LOP3 per word swaps every dropped
-        // expert half for the base half, so d = x - b is exactly +0 there (reference: k = 0, fusion.py:114)
-        static_assert(kFastPairs == 1 || kFastPairs == 2, "the keep-bit spread handles 2 or 4 elements per thread");
-        constexpr uint32_t kSpreadMask = (1u << kFastElems) - 1u;
-        constexpr uint32_t kSpreadMul = kFastPairs == 2 ? 0x10204080u : 0x4080u;
-        constexpr uint32_t kSpreadSign = kFastPairs == 2 ? 0x80808080u : 0x8080u;
-  static_assert(N <= 8, "output guard certified for N <= 11");
-        uint32_t spread[N];
+        // dropout on the integer side: 4 keep bits at a time go to the sign bits of 4 bytes (one IMAD by
+        // a per-thread multiplier that also picks the byte's low or high nibble; the other bits of the
+        // product are ignored), PRMT sign-replication turns them into halfword masks, and one LOP3 per
+        // word swaps every dropped expert half for the base half, so d = x - b is exactly +0 there
+        // (reference: k = 0, fusion.py:114)
+        static_assert(N <= 8, "output guard certified for N <= 10");
+        uint32_t spread[N][(kFastElems + 3) / 4];
 #pragma unroll
-        for (int i = 0; i < N; ++i) spread[i] = DROP ? (((kb[i] & kSpreadMask) * kSpreadMul) & kSpreadSign) : 0u;
+        for (int i = 0; i < N; ++i) {
+          if constexpr (kFastElems == 8) {
+            spread[i][0] = DROP ? (kb[i] & 0x0fu) * 0x10204080u : 0u;
+            spread[i][1] = DROP ? (kb[i] & 0xf0u) * 0x01020408u : 0u;
+          } else {
+            spread[i][0] = DROP ? (kb[i] & nib_mask) * nib_mul : 0u;
+          }
+        }
         uint32_t outw[kFastPairs];
-        float gm[kFastElems];  // signed guard margin per element: < 0 -> recompute exactly
+        uint32_t mx[kFastPairs];  // bf16x2(y - margin) ^ bf16x2(y + margin): non-zero half -> recompute
+        float gm[kFastPairs];     // vote / floor guard margin per pair: < 0 (or NaN) -> recompute both
 #pragma unroll
         for (int p = 0; p < kFastPairs; ++p) {
           const uint32_t bw = bw4.w[p];
@@ -916,7 +929,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 #pragma unroll
           for (int i = 0; i < N; ++i) {
             uint32_t xw = xw4[i].w[p];
-            if (DROP) xw = select_halves(xw, bw, prmt_sign(spread[i], p == 0 ? 0x9988u : 0xBBAAu));
+            if (DROP) xw = select_halves(xw, bw, prmt_sign(spread[i][p >> 1], (p & 1) ? 0xBBAAu : 0x9988u));
             const float2 d2 = bf16x2_minus_f32(xw, b2);
             k2[i] = __fmul2_rn(d2, make_float2(sr32[i], sr32[i]));
           }
@@ -982,14 +995,22 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
             y2 = b2;
 #pragma unroll
             for (int i = 0; i < N; ++i) y2 = __ffma2_rn(make_float2(w32[i], w32[i]), k2[i], y2);
+            // no vote margin: y * 0 is NaN exactly when y overflowed (inf or NaN), which the bracket
+            // below cannot see (a NaN y rounds both bracket ends to the same word)
+            g1 = __fmul2_rn(y2, make_float2(0.f, 0.f));
           }
-          // bf16 rounding must be certain: |y - midpoint| - 2^-20 * (|b| + max w * sum|k|) >= 0.  The f32
-          // evaluation error is <= (4 + N + 1) * 2^-24 * (|b| + max w * sum|k|): 3 roundings in k, 1 in w,
-          // N in the weighted sum, 1 in y -- so 2^-20 = 16 * 2^-24 is certified for N <= 11.
+          // bf16 rounding must be certain.  The f32 evaluation error is <= (4 + N + 1) * 2^-24 * S with
+          // S = |b| + max w * sum|k| (3 roundings in k, 1 in w, N in the weighted sum, 1 in y), so the
+          // reference's value lies in [y - 2^-20 S, y + 2^-20 S] (the two bracket ends are rounded once
+          // each, losing at most 2^-25 S of the 16 * 2^-24 S margin: certified for N <= 10).  RN to bf16 is
+          // monotone, so if both ends round to the same bf16 word, so does the reference's value -- the
+          // bracket covers the rounding boundaries on both sides of y, including the closer one below a
+          // power of two.  The output IS the lower end's word.
           const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, make_float2(fabsf(b2.x), fabsf(b2.y)));
-          const float2 mid = make_float2(mid_of(y2.x), mid_of(y2.y));
-          const float2 dm = __fadd2_rn(y2, make_float2(-mid.x, -mid.y));
-          const float2 g2 = __ffma2_rn(make_float2(-0x1p-20f, -0x1p-20f), S2, make_float2(fabsf(dm.x), fabsf(dm.y)));
+          const float2 ylo = __ffma2_rn(make_float2(-0x1p-20f, -0x1p-20f), S2, y2);
+          const float2 yhi = __ffma2_rn(make_float2(0x1p-20f, 0x1p-20f), S2, y2);
+          const uint32_t wlo = pack_bf16x2(ylo);
+          mx[p] = wlo ^ pack_bf16x2(yhi);
           // The bounds above are relative (normal-range rounding).  They also hold when S >= 2^-90: a
           // subnormal intermediate needs deltas below 2^-100, hence a base below 2^-93, hence S < 2^-90
           // (squared vote: k^2 must stay normal, i.e. |k| >= 2^-63, which S >= 2^-38 guarantees with
@@ -998,18 +1019,22 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
           constexpr float kInvFloor = ERASE == 2 ? 0x1p38f : 0x1p90f;
           // g3 = max(S / floor - 1, -S): < 0 exactly for 0 < S < floor (-0 for S == 0)
           const float2 g3a = __ffma2_rn(S2, make_float2(kInvFloor, kInvFloor), make_float2(-1.f, -1.f));
-          gm[2 * p] = fmin3_nan(g1.x, g2.x, fmaxf(g3a.x, -S2.x));
-          gm[2 * p + 1] = fmin3_nan(g1.y, g2.y, fmaxf(g3a.y, -S2.y));
-          __nv_bfloat162 p2 = __floats2bfloat162_rn(y2.x, y2.y);
-          outw[p] = *reinterpret_cast<uint32_t*>(&p2);
+          gm[p] = fmin4_nan(g1.x, g1.y, fmaxf(g3a.x, -S2.x), fmaxf(g3a.y, -S2.y));
+          outw[p] = wlo;
         }
         float gmin = gm[0];
 #pragma unroll
-        for (int e = 1; e < kFastElems; ++e) gmin = fmin_nan(gmin, gm[e]);
-        uint32_t slowm = 0;
-        if (!(gmin >= 0.f)) {  // negative or NaN
+        for (int q = 1; q < kFastPairs; ++q) gmin = fmin_nan(gmin, gm[q]);
+        uint32_t anym = mx[0];
 #pragma unroll
-          for (int e = 0; e < kFastElems; ++e) slowm |= (uint32_t)(!(gm[e] >= 0.f)) << e;
+        for (int q = 1; q < kFastPairs; ++q) anym |= mx[q];
+        uint32_t slowm = 0;
+        if (!(gmin >= 0.f) || anym != 0u) {  // a margin negative or NaN, or a bracket straddling a boundary
+#pragma unroll
+          for (int q = 0; q < kFastPairs; ++q) {
+            const uint32_t bad = !(gm[q] >= 0.f);
+            slowm |= ((bad | ((mx[q] & 0xffffu) != 0u)) << (2 * q)) | ((bad | ((mx[q] >> 16) != 0u)) << (2 * q + 1));
+          }
         }
         slowbits |= slowm << jit;
         FastVec::store(outp + out_base + le, outw);

@@ -357,33 +357,31 @@ class FusionCall:
             self.bitmap = torch.empty(self.n * self.words_per_row, dtype=torch.int32, device=self.device)
 
     # -- K1 + all_reduce + finalize
-    def norms(self, precomputed_sumsq: torch.Tensor | None = None) -> "FusionCall":
+    def norms(self) -> "FusionCall":
         s = L.stream_handle(self.stream)
         with torch.cuda.stream(self.stream):
-            if precomputed_sumsq is None:
-                world = 1
-                if self.group is not None:
-                    import torch.distributed as dist
-                    world = dist.get_world_size(self.group)
-                if self.partials is None or self.partials.numel() != self.layout.n_items * self.n:
-                    self.partials = torch.zeros(self.layout.n_items * self.n, dtype=torch.float64, device=self.device)
-                elif world > 1:
-                    self.partials.zero_()  # other ranks' slots must be exactly zero for the exact sum
-                self._bitmap(s)
-                seeds = (L.C.c_uint64 * self.n)(*self.seeds)
-                self._launch("rlk_fusion_sumsq", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
-                             int(self.delta_mode), L.ptr(self.partials), L.ptr(self.counters), self.dropout_mode,
-                             seeds, self.thresh, L.ptr(self.bitmap), self.words_per_row, s)
-                if self.group is not None:
-                    # disjoint slots: the sum is exact, so norms are identical at every world size
-                    from .dist import allreduce_partials
-                    allreduce_partials(self.partials, self.group)
-                self._launch("rlk_fusion_finalize", L.ptr(self.partials),
-                       L.ptr(self.layout.tensor_items_device(self.device, self.stream)), self.layout.n_tensors, self.n,
-                       self.cfg.target_mode, float(self.cfg.target_norm) if self.cfg.target_mode == 2 else 0.0,
-                       L.ptr(self.sumsq), L.ptr(self.scale), L.ptr(self.status), s)
-            else:
-                raise NotImplementedError
+            world = 1
+            if self.group is not None:
+                import torch.distributed as dist
+                world = dist.get_world_size(self.group)
+            if self.partials is None or self.partials.numel() != self.layout.n_items * self.n:
+                self.partials = torch.zeros(self.layout.n_items * self.n, dtype=torch.float64, device=self.device)
+            elif world > 1:
+                self.partials.zero_()  # other ranks' slots must be exactly zero for the exact sum
+            self._bitmap(s)
+            seeds = (L.C.c_uint64 * self.n)(*self.seeds)
+            self._launch("rlk_fusion_sumsq", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
+                         int(self.delta_mode), L.ptr(self.partials), L.ptr(self.counters), self.dropout_mode,
+                         seeds, self.thresh, L.ptr(self.bitmap), self.words_per_row, s)
+            if self.group is not None:
+                # disjoint slots: the sum is exact, so norms are identical at every world size
+                from .dist import allreduce_partials
+                allreduce_partials(self.partials, self.group)
+            self._launch("rlk_fusion_finalize", L.ptr(self.partials),
+                         L.ptr(self.layout.tensor_items_device(self.device, self.stream)), self.layout.n_tensors,
+                         self.n, self.cfg.target_mode,
+                         float(self.cfg.target_norm) if self.cfg.target_mode == 2 else 0.0,
+                         L.ptr(self.sumsq), L.ptr(self.scale), L.ptr(self.status), s)
         return self
 
     def check_status(self, per_tensor_raise: bool = True) -> torch.Tensor:

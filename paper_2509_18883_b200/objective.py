@@ -185,8 +185,12 @@ GRPO_WS_FLOATS_PER_ROW = 32  # K4a partials: (max, sum) per consumer warp (inclu
 class GRPOBatch:
     """Packed device-side description of a token batch (rows grouped by sample, samples by group).
 
-    sample_of_row[R] i32, tokens[R] i32, logp_train/logp_infer[R] f64, row_index[R] i64 or None,
-    per sample: adv, use (u8), temperature, norm = 1/(n_groups*G*T_max); group_rows[n_groups+1] i64."""
+    Per row: tokens i32, logp_train / logp_infer f64, sample_of_row i32 (local sample index),
+    row_index i64 or None.  Per local sample: adv, use (u8), temperature, norm = 1/(n_groups*G*T_max),
+    and sample_rows[S_local + 1] (row offsets).  A batch may hold a contiguous slice of the global
+    sample list (`select`, `shard`): `sample_base` is its first global sample and `group_samples`
+    [n_groups + 1] the global sample offsets of the groups, so per-sample token sums land at fixed
+    global slots and the objective is reduced in the same order at every world size."""
 
     tokens: torch.Tensor
     logp_train: torch.Tensor
@@ -196,15 +200,23 @@ class GRPOBatch:
     use: torch.Tensor
     temperature: torch.Tensor
     norm: torch.Tensor
-    group_rows: torch.Tensor
+    sample_rows: torch.Tensor
+    group_samples: torch.Tensor
     n_groups: int
     group_size: int
     t_max: int
+    n_samples: int
+    sample_base: int = 0
     row_index: torch.Tensor | None = None
+    sample_rows_host: tuple[int, ...] = ()
 
     @property
     def n_rows(self) -> int:
         return int(self.tokens.numel())
+
+    @property
+    def n_local_samples(self) -> int:
+        return int(self.adv.numel())
 
     def all_groups_seg(self) -> torch.Tensor:
         seg = getattr(self, "_all_seg", None)
@@ -237,9 +249,50 @@ class GRPOBatch:
             tokens=torch.as_tensor(tokens, dtype=torch.int32).to(dev).contiguous(),
             logp_train=f64(logp_train), logp_infer=f64(logp_infer), sample_of_row=sample_of_row,
             adv=f64(adv), use=torch.as_tensor(use, dtype=torch.uint8).to(dev).contiguous(), temperature=temp,
-            norm=norm, group_rows=cu[::group_size].to(dev).contiguous(), n_groups=n_groups,
-            group_size=group_size, t_max=t_max,
+            norm=norm, sample_rows=cu.to(dev).contiguous(),
+            group_samples=torch.arange(0, S + 1, group_size, dtype=torch.int64).to(dev), n_groups=n_groups,
+            group_size=group_size, t_max=t_max, n_samples=S, sample_rows_host=tuple(int(x) for x in cu),
             row_index=None if row_index is None else torch.as_tensor(row_index, dtype=torch.int64).to(dev))
+
+    def select(self, s0: int, s1: int) -> "GRPOBatch":
+        """The sub-batch of local samples [s0, s1) (their rows, same global normalisation): a response
+        shard of a rank, or a chunk streamed through one logits buffer."""
+        S = self.n_local_samples
+        if not 0 <= s0 <= s1 <= S:
+            raise IndexError(f"sample range [{s0}, {s1}) outside [0, {S})")
+        cu = self.sample_rows_host
+        r0, r1 = cu[s0], cu[s1]
+        rows = slice(r0, r1)
+        sub_cu = tuple(c - r0 for c in cu[s0:s1 + 1])
+        return GRPOBatch(
+            tokens=self.tokens[rows], logp_train=self.logp_train[rows], logp_infer=self.logp_infer[rows],
+            sample_of_row=(self.sample_of_row[rows] - s0).contiguous(), adv=self.adv[s0:s1],
+            use=self.use[s0:s1], temperature=self.temperature[s0:s1], norm=self.norm[s0:s1],
+            sample_rows=torch.tensor(sub_cu, dtype=torch.int64, device=self.tokens.device),
+            group_samples=self.group_samples, n_groups=self.n_groups, group_size=self.group_size,
+            t_max=self.t_max, n_samples=self.n_samples, sample_base=self.sample_base + s0,
+            row_index=None if self.row_index is None else self.row_index[rows], sample_rows_host=sub_cu)
+
+    def shard_bounds(self, world: int) -> list[int]:
+        """Sample boundaries of `world` contiguous shards balanced by row count (the loss
+        shards by response; a rank may get none)."""
+        cu = self.sample_rows_host
+        R = cu[-1]
+        bounds = [0]
+        for r in range(1, world):
+            target = R * r / world
+            # first sample boundary at or after the target row count, never moving backwards
+            k = bounds[-1]
+            while k < len(cu) - 1 and cu[k] < target:
+                k += 1
+            bounds.append(k)
+        bounds.append(len(cu) - 1)
+        return bounds
+
+    def shard(self, world: int, rank: int) -> "GRPOBatch":
+        """This rank's contiguous share of the samples (`shard_bounds`)."""
+        b = self.shard_bounds(world)
+        return self.select(b[rank], b[rank + 1])
 
 
 @dataclass
@@ -251,14 +304,47 @@ class GRPOForward:
     term: torch.Tensor
     coef: torch.Tensor
     flags: torch.Tensor
+    sample_sums: torch.Tensor | None = None  # [n_local_samples] f64: this batch's per-sample sums
+
+
+def grpo_objective(sample_sums: torch.Tensor, batch: GRPOBatch, group=None, *, stream=None) -> tuple:
+    """J from per-sample token sums: the sums go to their global slots of an [n_samples] vector (zero
+    elsewhere), which is all-reduced over `group` -- every slot has exactly one non-zero contributor,
+    so the sum is exact -- then summed per group in a fixed order, / (G T_max), averaged over groups
+    (objective.py:237-250).  J is therefore bit-identical at every world size.  Returns (J, group sums)."""
+    dev = sample_sums.device
+    f64 = dict(dtype=torch.float64, device=dev)
+    s = L.stream_handle(stream)
+    if batch.sample_base == 0 and sample_sums.numel() == batch.n_samples and group is None:
+        full = sample_sums
+    else:
+        full = torch.zeros(batch.n_samples, **f64)
+        full[batch.sample_base:batch.sample_base + sample_sums.numel()] = sample_sums
+    if group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(full, group=group)
+    gs = torch.empty(batch.n_groups, **f64)
+    L.call("rlk_segment_sum_f64", L.ptr(full), L.ptr(batch.group_samples), batch.n_groups, L.ptr(gs), s)
+    scaled = gs / float(batch.group_size * batch.t_max)
+    tot = torch.empty(1, **f64)
+    L.call("rlk_segment_sum_f64", L.ptr(scaled), L.ptr(batch.all_groups_seg()), 1, L.ptr(tot), s)
+    return tot[0] / batch.n_groups, gs
+
+
+def _finish(term: torch.Tensor, batch: GRPOBatch, group, s) -> tuple:
+    ss = torch.empty(batch.n_local_samples, dtype=torch.float64, device=term.device)
+    L.call("rlk_segment_sum_f64", L.ptr(term), L.ptr(batch.sample_rows), batch.n_local_samples, L.ptr(ss), s)
+    J, gs = grpo_objective(ss, batch, group)
+    return J, gs, ss
 
 
 def grpo_forward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = ClipConfig(), *, stream=None,
                  group=None) -> GRPOForward:
-    """K4 over every row + fixed-order per-group sums; J = sum_g (S_g / (G T_max)) / n_groups.
+    """K4 over every row + fixed-order per-sample then per-group sums; J = sum_g (S_g / (G T_max)) / n_groups.
 
-    `logits` is [rows, V] (row_stride = V) in bf16/f32/f64.  With a process group, rows are this
-    rank's share and the per-group sums are all-reduced (one f64 vector)."""
+    `logits` is [rows, V] (row_stride = V) in bf16/f32/f64.  With a process group, `batch` is this
+    rank's share of the samples (`GRPOBatch.shard`) and the per-sample sums are all-reduced (one f64
+    vector of n_samples entries); without one, a partial batch gives its own samples' share of J."""
     if logits.ndim != 2:
         raise ValueError("logits must be [rows, vocab]")
     if stream is not None:
@@ -277,15 +363,8 @@ def grpo_forward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = Clip
            L.ptr(batch.tokens), L.ptr(batch.logp_train), L.ptr(batch.logp_infer), L.ptr(batch.sample_of_row),
            L.ptr(batch.adv), L.ptr(batch.use), L.ptr(batch.temperature), L.ptr(batch.norm), L.C.byref(c),
            L.ptr(logp), L.ptr(lse), L.ptr(term), L.ptr(coef), L.ptr(flags), L.ptr(ws), ws.numel(), s)
-    gs = torch.empty(batch.n_groups, **f64)
-    L.call("rlk_segment_sum_f64", L.ptr(term), L.ptr(batch.group_rows), batch.n_groups, L.ptr(gs), s)
-    if group is not None:
-        import torch.distributed as dist
-        dist.all_reduce(gs, group=group)
-    scaled = gs / float(batch.group_size * batch.t_max)
-    tot = torch.empty(1, **f64)
-    L.call("rlk_segment_sum_f64", L.ptr(scaled), L.ptr(batch.all_groups_seg()), 1, L.ptr(tot), s)
-    return GRPOForward(tot[0] / batch.n_groups, gs, logp, lse, term, coef, flags)
+    J, gs, ss = _finish(term, batch, group, s)
+    return GRPOForward(J, gs, logp, lse, term, coef, flags, ss)
 
 
 def _row_csr(row_index: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
@@ -299,15 +378,17 @@ def _row_csr(row_index: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch
 
 
 def grpo_backward(logits: torch.Tensor, batch: GRPOBatch, fwd: GRPOForward, grad_scale: torch.Tensor | float = 1.0,
-                  grad_dtype: torch.dtype | None = None, *, stream=None) -> torch.Tensor:
+                  grad_dtype: torch.dtype | None = None, *, stream=None, group=None) -> torch.Tensor:
     """K5: grad_scale * dJ/dlogits, same shape as `logits` (the autograd grad_out is `grad_scale`).
 
     Without `row_index`, token r reads logits row r (the batch's rows must not exceed the logits'; rows
-    past the batch get a zero gradient).  With `row_index`, every distinct row read is written once as
-    the sum over the tokens that read it (CSR), and rows no token reads are zero (objective.py:253-283)."""
+    past the batch get a zero gradient) and a sharded batch needs no communication.  With `row_index`,
+    every distinct row read is written once as the sum over the tokens that read it (CSR), and rows no
+    token reads are zero (objective.py:253-283); with a process group the shared table's gradient is
+    then summed over the ranks (all_reduce)."""
     if stream is not None:
         with torch.cuda.stream(stream):
-            return grpo_backward(logits, batch, fwd, grad_scale, grad_dtype)
+            return grpo_backward(logits, batch, fwd, grad_scale, grad_dtype, group=group)
     if logits.ndim != 2:
         raise ValueError("logits must be [rows, vocab]")
     logits = logits.contiguous()
@@ -332,12 +413,14 @@ def grpo_backward(logits: torch.Tensor, batch: GRPOBatch, fwd: GRPOForward, grad
     if nb and (int(ri.min()) < 0 or int(ri.max()) >= R):
         raise IndexError(f"row_index out of range [0, {R})")
     grad = torch.zeros((R, V), dtype=gdt, device=logits.device)
-    if nb == 0:
-        return grad
-    rows, ptr_, order = _row_csr(ri)
-    L.call("rlk_grpo_bwd", L.ptr(logits), L.dtype_code(logits.dtype), rows.numel(), V, V, L.ptr(rows), L.ptr(ptr_),
-           L.ptr(order), L.ptr(batch.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(coef), L.ptr(grad),
-           L.dtype_code(grad.dtype), V, s)
+    if nb:
+        rows, ptr_, order = _row_csr(ri)
+        L.call("rlk_grpo_bwd", L.ptr(logits), L.dtype_code(logits.dtype), rows.numel(), V, V, L.ptr(rows),
+               L.ptr(ptr_), L.ptr(order), L.ptr(batch.tokens), L.ptr(temp_tok), L.ptr(fwd.lse), L.ptr(coef),
+               L.ptr(grad), L.dtype_code(grad.dtype), V, s)
+    if group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(grad, group=group)
     return grad
 
 
@@ -352,7 +435,7 @@ def grpo_forward_backward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConf
     R, V = logits.shape
     if logits.dtype != torch.bfloat16 or batch.row_index is not None or V % 16 or V > 204800:
         fwd = grpo_forward(logits, batch, clip, group=group)
-        return fwd, grpo_backward(logits, batch, fwd, grad_scale)
+        return fwd, grpo_backward(logits, batch, fwd, grad_scale, group=group)
     dev = logits.device
     f64 = dict(dtype=torch.float64, device=dev)
     logp, lse, term, coef = (torch.empty(R, **f64) for _ in range(4))
@@ -364,15 +447,8 @@ def grpo_forward_backward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConf
            L.ptr(batch.logp_infer), L.ptr(batch.sample_of_row), L.ptr(batch.adv), L.ptr(batch.use),
            L.ptr(batch.temperature), L.ptr(batch.norm), L.C.byref(c), float(grad_scale), L.ptr(logp), L.ptr(lse),
            L.ptr(term), L.ptr(coef), L.ptr(flags), L.ptr(grad), V, s)
-    gs = torch.empty(batch.n_groups, **f64)
-    L.call("rlk_segment_sum_f64", L.ptr(term), L.ptr(batch.group_rows), batch.n_groups, L.ptr(gs), s)
-    if group is not None:
-        import torch.distributed as dist
-        dist.all_reduce(gs, group=group)
-    scaled = gs / float(batch.group_size * batch.t_max)
-    tot = torch.empty(1, **f64)
-    L.call("rlk_segment_sum_f64", L.ptr(scaled), L.ptr(batch.all_groups_seg()), 1, L.ptr(tot), s)
-    return GRPOForward(tot[0] / batch.n_groups, gs, logp, lse, term, coef, flags), grad
+    J, gs, ss = _finish(term, batch, group, s)
+    return GRPOForward(J, gs, logp, lse, term, coef, flags, ss), grad
 
 
 class GRPOTokenLoss(torch.autograd.Function):
@@ -455,7 +531,7 @@ def _pack_masked_batch(batch: MaskedBatch, params: ParamTable) -> tuple[GRPOBatc
     """USE samples' tokens -> packed rows reading logits row context_id * max_len + t."""
     V, T = params.vocab_size, params.max_len
     toks, lt, li, rows, cu, adv, temps = [], [], [], [], [0], [], []
-    group_rows = [0]
+    group_samples = [0]
     for mg in batch.groups:
         for sample, a, mask in zip(mg.group.samples, mg.advantages, mg.masks):
             if mask is not Mask.USE:
@@ -484,7 +560,7 @@ def _pack_masked_batch(batch: MaskedBatch, params: ParamTable) -> tuple[GRPOBatc
             cu.append(len(toks))
             adv.append(float(a))
             temps.append(float(tau))
-        group_rows.append(len(cu) - 1)
+        group_samples.append(len(cu) - 1)
     lt_a, li_a = np.asarray(lt, dtype=np.float64), np.asarray(li, dtype=np.float64)
     if not (np.isfinite(lt_a).all() and np.isfinite(li_a).all()):
         raise ValueError("log-probs must be finite")
@@ -501,8 +577,8 @@ def _pack_masked_batch(batch: MaskedBatch, params: ParamTable) -> tuple[GRPOBatc
         use=torch.ones(S, dtype=torch.uint8, device=dev),
         temperature=torch.tensor(temps, dtype=torch.float64, device=dev),
         norm=torch.full((S,), 1.0 / (n_groups * G * batch.t_max), dtype=torch.float64, device=dev),
-        group_rows=torch.tensor([cu[g] for g in group_rows], dtype=torch.int64, device=dev),
-        n_groups=n_groups, group_size=G, t_max=batch.t_max,
+        sample_rows=cu_t.to(dev), group_samples=torch.tensor(group_samples, dtype=torch.int64, device=dev),
+        n_groups=n_groups, group_size=G, t_max=batch.t_max, n_samples=S, sample_rows_host=tuple(cu),
         row_index=torch.tensor(rows, dtype=torch.int64, device=dev))
     return b, rows
 

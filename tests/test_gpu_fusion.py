@@ -343,3 +343,72 @@ def test_fast_path_adversarial_values(cuda, monkeypatch):
         got = outs[0][0].view(torch.int16).cpu().numpy().view(np.uint16)
         assert int((got != rne_bf16_bits(ref)).sum()) == 0, cfgkw
         assert list(rep.stats("w").erased_counts) == st["erased"], cfgkw
+
+
+def test_fast_path_power_of_two_boundaries(cuda):
+    """Results just below / above a power of two under heavy cancellation (S ~ 2^11..2^12 |y|): the
+    bf16 rounding boundary below 2^E sits at 2^E - 2^(E-9), a quarter of the upper ulp away, so a
+    guard that only measures the distance to the upper midpoint would accept an f32 value above 2^E
+    whose reference value rounds down.  The certified fast path (bracket [y - 2^-20 S, y + 2^-20 S]
+    must round to one word) must equal the reference-order f64 path and RNE_bf16(oracle)."""
+    from paper_2509_18883_b200 import fusion as F
+    g = np.random.default_rng(5)
+    n = 1 << 22
+    # four experts: two huge cancelling deltas, then two finer ones steering the result onto the
+    # boundary below 2^E (the last expert's granularity puts y within ~2^(E-10) of the target)
+    w = np.array([0.4, 0.3, 0.2, 0.1])
+    E = g.integers(-12, 12, n).astype(np.float64)
+    p2 = 2.0 ** E
+    base = bf16_round(p2 * (1 + g.integers(-4, 5, n) * 2.0 ** -8))
+    target = p2 * (1 - 2.0 ** -9 * (1 + g.uniform(-2.0 ** -6, 2.0 ** -6, n)))  # the boundary below 2^E
+    A = p2 * 2.0 ** g.uniform(10.5, 12.0, n)
+    experts, acc = [], base.copy()
+    e0 = bf16_round(base + A)
+    experts.append(e0)
+    acc += w[0] * (e0 - base)
+    experts.append(bf16_round(base - w[0] * (e0 - base) / w[1]))
+    acc += w[1] * (experts[1] - base)
+    for i in (2, 3):
+        experts.append(bf16_round(base + (target - acc) / w[i]))
+        acc += w[i] * (experts[i] - base)
+    bt = torch.from_numpy(base).to(cuda, torch.bfloat16)
+    ets = [torch.from_numpy(e).to(cuda, torch.bfloat16) for e in experts]
+    cfgkw = dict(target_norm=None, erase_mode=False, merge_weights=tuple(w))
+    outs = []
+    for exact in (False, True):
+        o, _ = F.fuse_state_dict({"w": bt}, [{"w": e} for e in ets], F.FusionConfig(**cfgkw), exact_merge=exact)
+        outs.append(o["w"].clone())
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    ref, _ = OF.fuse(base, experts, **cfgkw)
+    got = outs[0].view(torch.int16).cpu().numpy().view(np.uint16)
+    assert int((got != rne_bf16_bits(ref)).sum()) == 0
+    near = np.abs(ref - p2 * (1 - 2.0 ** -9)) < 2.0 ** -14 * p2
+    assert near.sum() > n // 4  # the construction really lands on the boundary
+
+
+def test_fast_path_overflow_falls_back(cuda):
+    """Deltas beyond the f32 range (|e - b| > 3.4e38) make the f32 merge produce inf, or NaN through a
+    zero weight times an infinite delta; with the erase vote off there is no vote margin to catch it,
+    so the fast path must still send those elements to the exact f64 path (the reference never
+    overflows in float64)."""
+    from paper_2509_18883_b200 import fusion as F
+    g = np.random.default_rng(8)
+    n = 1 << 16
+    base = bf16_round(g.choice([-1.0, 1.0], n) * 10.0 ** g.uniform(37.5, 38.4, n))
+    experts = [bf16_round(-base * g.uniform(0.5, 1.0, n)), bf16_round(-base * 0.9), bf16_round(base * 0.5)]
+    small = g.random(n) < 0.5  # half the columns stay in range
+    for e in experts:
+        e[small] = bf16_round(base[small] * 1.01)
+    bt = torch.from_numpy(base).to(cuda, torch.bfloat16)
+    ets = [torch.from_numpy(e).to(cuda, torch.bfloat16) for e in experts]
+    for cfgkw in (dict(target_norm=None, erase_mode=False, merge_weights=(1.0, 0.0, 0.0)),
+                  dict(target_norm=None, erase_mode=False, merge_weights=(0.5, 0.3, 0.2))):
+        outs = []
+        for exact in (False, True):
+            o, _ = F.fuse_state_dict({"w": bt}, [{"w": e} for e in ets], F.FusionConfig(**cfgkw),
+                                     exact_merge=exact)
+            outs.append(o["w"].clone())
+        assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16)), cfgkw
+        ref, _ = OF.fuse(base, experts, **cfgkw)
+        got = outs[0].view(torch.int16).cpu().numpy().view(np.uint16)
+        assert int((got != rne_bf16_bits(ref)).sum()) == 0, cfgkw

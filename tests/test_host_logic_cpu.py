@@ -107,3 +107,33 @@ def test_apply_masks_branches_match_reference(cname):
     for g, u in enumerate(usable):
         if u < 2:
             assert all(s["adv"] == 0.0 for s in meta["samples"][g * G:(g + 1) * G])
+
+
+def test_grpo_batch_shard_and_select_cpu():
+    """GRPOBatch.shard: contiguous sample ranges balanced by rows, covering every sample once, with the
+    global normalisation and sample slots kept (the all-reduce of per-sample sums relies on it)."""
+    import numpy as np
+    import torch
+    from paper_2509_18883_b200 import objective as O
+    lens = [7, 0, 3, 12, 1, 9, 4, 4]
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    R = int(cu[-1])
+    b = O.GRPOBatch.pack(np.arange(R), np.zeros(R), np.zeros(R), cu, np.arange(8.0), np.ones(8, np.uint8), 4, 12,
+                         device=torch.device("cpu"))
+    for world in (1, 2, 3, 4, 8, 11):
+        bounds = b.shard_bounds(world)
+        assert bounds[0] == 0 and bounds[-1] == 8 and bounds == sorted(bounds) and len(bounds) == world + 1
+        rows = []
+        for r in range(world):
+            s = b.shard(world, r)
+            assert s.sample_base == bounds[r] and s.n_samples == 8 and s.n_groups == 2
+            assert s.n_local_samples == bounds[r + 1] - bounds[r]
+            assert torch.equal(s.adv, b.adv[bounds[r]:bounds[r + 1]])
+            assert torch.equal(s.norm, b.norm[bounds[r]:bounds[r + 1]])
+            assert s.sample_rows_host[0] == 0 and s.sample_rows_host[-1] == s.n_rows
+            if s.n_rows:
+                assert int(s.sample_of_row.min()) >= 0 and int(s.sample_of_row.max()) < s.n_local_samples
+            rows.extend(s.tokens.tolist())
+        assert rows == list(range(R))
+    with pytest.raises(IndexError):
+        b.select(3, 9)
