@@ -25,13 +25,49 @@ template <int N> struct StreamBytes { static constexpr uint32_t v = N <= 4 ? 819
 
 struct ItemGeom {
   const rlk_fusion_segment* seg;
+  uint64_t j0;  // seg->j0 (cached)
+  void* out;    // seg->out (cached)
   uint64_t start;  // element offset of the item within its piece
   uint32_t len;
   uint32_t gitem;
   uint32_t tensor;
 };
 
-__device__ __forceinline__ ItemGeom item_geom(const rlk_fusion_plan& plan, uint32_t item) {
+// Items of a CTA are visited in increasing order (item += gridDim.x) and segments are in item order,
+// so the segment of the next item is found by a forward scan from the current one, and the
+// segment's fields are re-read only when it changes: one item's geometry costs no global loads in
+// the common case, instead of a dependent binary search (~log2(n_segs) L2 round trips) per item.
+struct SegCursor {
+  uint32_t lo = 0xffffffffu;  // current segment (none yet)
+  uint32_t p_lo = 0, p_hi = 0;  // seg_item_prefix[lo], seg_item_prefix[lo + 1]
+  const rlk_fusion_segment* seg = nullptr;
+  uint64_t numel = 0, j0 = 0;
+  void* out = nullptr;
+  uint32_t item0 = 0, tensor = 0;
+  // moves to the segment holding `item`; returns true when it changed
+  __device__ __forceinline__ bool seek(const rlk_fusion_plan& plan, uint32_t item) {
+    if (lo != 0xffffffffu && item < p_hi) return false;
+    if (lo == 0xffffffffu) {
+      lo = 0;
+      p_lo = __ldg(plan.seg_item_prefix);
+      p_hi = __ldg(plan.seg_item_prefix + 1);
+    }
+    while (item >= p_hi) {
+      ++lo;
+      p_lo = p_hi;
+      p_hi = __ldg(plan.seg_item_prefix + lo + 1);
+    }
+    seg = plan.segs + lo;
+    numel = seg->numel;
+    j0 = seg->j0;
+    out = seg->out;
+    item0 = seg->item0;
+    tensor = seg->tensor;
+    return true;
+  }
+};
+
+__device__ __forceinline__ ItemGeom item_geom_bs(const rlk_fusion_plan& plan, uint32_t item) {
   uint32_t lo = 0, hi = plan.n_segs;
   while (hi - lo > 1) {
     uint32_t mid = (lo + hi) >> 1;
@@ -39,6 +75,8 @@ __device__ __forceinline__ ItemGeom item_geom(const rlk_fusion_plan& plan, uint3
   }
   ItemGeom g;
   g.seg = plan.segs + lo;
+  g.j0 = g.seg->j0;
+  g.out = g.seg->out;
   uint32_t k = item - __ldg(plan.seg_item_prefix + lo);
   g.start = (uint64_t)k * kItem;
   uint64_t rem = g.seg->numel - g.start;
@@ -48,9 +86,26 @@ __device__ __forceinline__ ItemGeom item_geom(const rlk_fusion_plan& plan, uint3
   return g;
 }
 
+__device__ __forceinline__ ItemGeom item_geom(const rlk_fusion_plan& plan, SegCursor& c, uint32_t item) {
+  c.seek(plan, item);
+  ItemGeom g;
+  g.seg = c.seg;
+  g.j0 = c.j0;
+  g.out = c.out;
+  const uint32_t k = item - c.p_lo;
+  g.start = (uint64_t)k * kItem;
+  const uint64_t rem = c.numel - g.start;
+  g.len = rem < kItem ? (uint32_t)rem : kItem;
+  g.gitem = c.item0 + k;
+  g.tensor = c.tensor;
+  return g;
+}
+
 // Producer: one elected lane streams every (item, stage) of this CTA through the ring.
 // Stage layout: [stream 0 | stream 1 | ... | stream NS-1 | bitmap expert 0 | ... | bitmap expert N-1].
-template <int ESZ, int N, uint32_t SB = StreamBytes<N>::v>
+// kCursor: item geometry from the incremental SegCursor (K3: its per-item stalls cost bandwidth) or a
+// binary search per item (K1: measured faster there, same-box A/B)
+template <int ESZ, int N, uint32_t SB = StreamBytes<N>::v, bool kCursor = true>
 __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_base, const uint32_t* bitmap,
                         uint64_t words_per_row) {
   constexpr uint32_t ELEMS = SB / ESZ;
@@ -62,8 +117,9 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
   const uint64_t pol = policy_evict_first();
   const uint64_t pol_bm = policy_evict_last();
   RingPos q;
+  SegCursor cur;
   for (uint32_t item = blockIdx.x; item < plan.n_items; item += gridDim.x) {
-    const ItemGeom g = item_geom(plan, item);
+    const ItemGeom g = kCursor ? item_geom(plan, cur, item) : item_geom_bs(plan, item);
     const char* src[N + 1];
     if (!with_base) {
 #pragma unroll
@@ -73,7 +129,7 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
 #pragma unroll
       for (int i = 0; i < N; ++i) src[i + 1] = (const char*)g.seg->expert[i];
     }
-    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    const uint64_t jtensor0 = g.j0 + g.start;
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_bytes = (n * ESZ) & ~15u;
@@ -196,16 +252,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ S
   const bool count = a.counters != nullptr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kCWarps) {
-    if (lane == 0) produce<ESZ, N>(a.plan, r, !delta, (count && a.dropout_mode == 2) ? a.bitmap : nullptr,
+    if (lane == 0) produce<ESZ, N, StreamBytes<N>::v, false>(a.plan, r, !delta, (count && a.dropout_mode == 2) ? a.bitmap : nullptr,
                                    a.words_per_row);
     return;
   }
   __shared__ double red[kCWarps][N];
   const int tid = threadIdx.x;
   RingPos q;
+  SegCursor cur;
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
-    const ItemGeom g = item_geom(a.plan, item);
-    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    const ItemGeom g = item_geom(a.plan, cur, item);
+    const uint64_t jtensor0 = g.j0 + g.start;
     double acc[N][2];
     uint32_t nz[N];
 #pragma unroll
@@ -300,15 +357,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq_bf16(const __grid_constan
   const Ring r = ring_setup(smem, a.stage_bytes, a.nstages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kCWarps) {
-    if (lane == 0) produce<2, N>(a.plan, r, true, COUNT == 2 ? a.bitmap : nullptr, a.words_per_row);
+    if (lane == 0) produce<2, N, StreamBytes<N>::v, false>(a.plan, r, true, COUNT == 2 ? a.bitmap : nullptr, a.words_per_row);
     return;
   }
   __shared__ double red[kCWarps][N];
   const int tid = threadIdx.x;
   RingPos q;
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
-    const ItemGeom g = item_geom(a.plan, item);
-    const uint64_t jtensor0 = g.seg->j0 + g.start;
+        const ItemGeom g = item_geom_bs(a.plan, item);
+    const uint64_t jtensor0 = g.j0 + g.start;
     double acc0[N], acc1[N];
     uint32_t nz[N];
 #pragma unroll
@@ -643,8 +700,9 @@ __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid
   }
   const int tid = threadIdx.x;
   RingPos q;
+  SegCursor cur;
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
-    const ItemGeom g = item_geom(a.plan, item);
+    const ItemGeom g = item_geom(a.plan, cur, item);
     const double* scale = a.scale + (uint64_t)g.tensor * N;
     ElemConsts c;
 #pragma unroll
@@ -652,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid
     uint32_t cnt_er[N];  // entries erased (non-zero entries after dropout are counted by K1)
 #pragma unroll
     for (int i = 0; i < N; ++i) cnt_er[i] = 0;
-    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    const uint64_t jtensor0 = g.j0 + g.start;
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_elems = ((n * ESZ) & ~15u) / ESZ;
@@ -686,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid
 #pragma unroll
             for (int i = 0; i < N; ++i) cnt_er[i] += (erm >> i) & 1u;
           }
-          store_vec_f64<DTO, VEC>(g.seg->out, out_base + le, y);
+          store_vec_f64<DTO, VEC>(g.out, out_base + le, y);
         }
       }
       // tail elements (fewer than 16 bytes) straight from global memory
@@ -707,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid
 #pragma unroll
         for (int i = 0; i < N; ++i) cnt_er[i] += (erm >> i) & 1u;
         (void)nzm;
-        store_from_f64<DTO>(g.seg->out, idx, Y);
+        store_from_f64<DTO>(g.out, idx, Y);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[s]);
@@ -783,9 +841,6 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float2 v) {
   __nv_bfloat162 p = __floats2bfloat162_rn(v.x, v.y);
   return *reinterpret_cast<uint32_t*>(&p);
 }
-__device__ __forceinline__ float fmin4_nan(float a, float b, float c, float d) {
-  return fmin_nan(fmin3_nan(a, b, c), d);
-}
 
 // Fast K3 for bf16 experts + bf16 base -> bf16 (the checkpoint path): f32x2 arithmetic with certified
 // guards; DROP 0 = no dropout, 2 = keep bits from the K2 bitmap; ERASE 0 off, 1 sum vote, 2 squared vote.
@@ -851,33 +906,52 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
   const uint32_t nib_mask = (tid & 1) ? 0xf0u : 0x0fu;
   const uint32_t nib_mul = (tid & 1) ? 0x01020408u : 0x10204080u;
   const float cv = ERASE == 1 ? 0x1p-20f : 0x1p-19f;
+  // Scaled domain (ERASE 0 / 1): the kernel works with k' = k * 2^24 and folds 2^-24 into the weights
+  // (both exact power-of-two scalings).  Every non-zero k' is then a normal float (|d| >= 2^-133,
+  // sr >= 2^-16), so its rounding error is relative, and the vote's partial sums are either normal or
+  // subnormal-and-exact: the vote's relative error bound needs no subnormal guard.  What can still be
+  // tiny are the weighted terms of y, covered by the 2^-110 floor in S below.  The squared vote
+  // (ERASE 2) would square the scale: it keeps k unscaled and its own floor check.
+  constexpr float kKS = ERASE == 2 ? 1.f : 0x1p24f;
+  constexpr float kKSinv = ERASE == 2 ? 1.f : 0x1p-24f;
   float w32[N], wh32[N];
   float wmax = 0.f;
+  bool w_ok = true;  // w * 2^-24 exact and normal: every weight zero or >= 2^-100
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    w32[i] = (float)a.w[i];
+    const float w = (float)a.w[i];
+    w_ok = w_ok && (w == 0.f || w >= 0x1p-100f);
+    w32[i] = w * kKSinv;
     wh32[i] = 0.5f * w32[i];
     wmax = fmaxf(wmax, w32[i]);
   }
   RingPos q;
+  SegCursor cur;
+  ElemConsts c;
+  float sr32[N];
+  bool fast_ok = false;
+  uint32_t c_tensor = 0xffffffffu;  // tensor whose scales are loaded
   for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
-    const ItemGeom g = item_geom(a.plan, item);
+    const ItemGeom g = item_geom(a.plan, cur, item);
     const double* scale = a.scale + (uint64_t)g.tensor * N;
-    uint16_t* const outp = (uint16_t*)g.seg->out;
-    ElemConsts c;
-    float sr32[N];
-    bool fast_ok = true;
+    uint16_t* const outp = (uint16_t*)g.out;
+    if (g.tensor != c_tensor) {  // per-tensor constants: reloaded only when the tensor changes
+      c_tensor = g.tensor;
+      fast_ok = w_ok;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      c.scale[i] = __ldg(scale + i);
-      sr32[i] = (float)(DROP ? c.scale[i] / a.keep_prob : c.scale[i]);
-      // k = d * sr cannot underflow for bf16 deltas (|d| >= 2^-133) when sr >= 2^-16
-      fast_ok = fast_ok && sr32[i] >= 0x1p-16f && sr32[i] < 0x1p100f;
+      for (int i = 0; i < N; ++i) {
+        c.scale[i] = __ldg(scale + i);
+        sr32[i] = (float)(DROP ? c.scale[i] / a.keep_prob : c.scale[i]);
+        // k = d * sr cannot underflow for bf16 deltas (|d| >= 2^-133) when sr >= 2^-16; sr < 2^100
+        // keeps sr * 2^24 finite
+        fast_ok = fast_ok && sr32[i] >= 0x1p-16f && sr32[i] < 0x1p100f;
+        sr32[i] *= kKS;
+      }
     }
     uint32_t cnt_er[N];  // entries erased (non-zero entries after dropout are counted by K1)
 #pragma unroll
     for (int i = 0; i < N; ++i) cnt_er[i] = 0;
-    const uint64_t jtensor0 = g.seg->j0 + g.start;
+    const uint64_t jtensor0 = g.j0 + g.start;
     for (uint32_t off = 0; off < g.len; off += ELEMS) {
       const uint32_t n = min(ELEMS, g.len - off);
       const uint32_t main_elems = ((n * 2) & ~15u) / 2;
@@ -887,12 +961,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
       const uint8_t* bm = sb + (N + 1) * SB;
       const uint32_t nvec = main_elems / kFastElems;
       const uint64_t out_base = g.start + off;
-      // elements whose guard trips are only recorded here (bit 4 j + e: iteration j, element e) and
-      // recomputed after the stage's fast loop, so the hot loop carries no slow-path code and a warp
-      // pays max-over-lanes(popcount) slow rounds per stage, not one per element position per iteration
+      // elements whose guard trips are only recorded here (bit kFastElems * j + e: iteration j, element
+      // e) and recomputed after the stage's fast loop, so the hot loop carries no slow-path code and a
+      // warp pays max-over-lanes(popcount) slow rounds per stage, not one per element position
       static_assert(ELEMS / kFastElems / kFastCThreads * kFastElems <= 32, "slow bits per stage exceed a word");
-      uint32_t slowbits = 0, jit = 0;
-      for (uint32_t v = fast_ok ? tid : nvec; v < nvec; v += kFastCThreads, jit += kFastElems) {
+      uint32_t slowbits = 0;
+      auto vec = [&](const uint32_t v, const uint32_t jit) {
         const uint32_t le = v * kFastElems;
         const FastVec bw4 = FastVec::load(sb + v * (2 * kFastElems));
         FastVec xw4[N];
@@ -920,7 +994,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         }
         uint32_t outw[kFastPairs];
         uint32_t mx[kFastPairs];  // bf16x2(y - margin) ^ bf16x2(y + margin): non-zero half -> recompute
-        float gm[kFastPairs];     // vote / floor guard margin per pair: < 0 (or NaN) -> recompute both
+        float gm[kFastPairs];     // vote / overflow margin per pair: < 0 (or NaN) -> recompute both
 #pragma unroll
         for (int p = 0; p < kFastPairs; ++p) {
           const uint32_t bw = bw4.w[p];
@@ -942,26 +1016,35 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 #pragma unroll
             for (int i = 2; i < N; ++i) aa = __fadd2_rn(aa, make_float2(fabsf(k2[i].x), fabsf(k2[i].y)));
           }
-          float2 y2, g1 = make_float2(1.f, 1.f);
+          // S = |b| + max w * sum|k| (+ 2^-110 in the scaled domain): a subnormal weighted term of y adds
+          // at most 2^-150 absolute per rounding (N + 2 of them), which the floor covers with room to
+          // spare (2^-20 S >= 2^-130 in the output bracket).  Overflow makes S infinite.
+          float2 babs = make_float2(fabsf(b2.x), fabsf(b2.y));
+          if constexpr (ERASE != 2) babs = __fadd2_rn(babs, make_float2(0x1p-110f, 0x1p-110f));
+          const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, babs);
+          float2 y2, g1;
           if constexpr (kErase) {
-            float2 vv, gg;
+            float2 vv;
             if (ERASE == 1) {
               vv = k2[0];
 #pragma unroll
               for (int i = 1; i < N; ++i) vv = __fadd2_rn(vv, k2[i]);
-              gg = aa;
+              // |vote| - 2^-20 sum|k'| (one rounding: its sign is exact).  < 0: the f32 vote's sign is not
+              // certain (its error is <= 6 * 2^-24 sum|k'|, all of it relative: no subnormals in the
+              // scaled domain); NaN: an overflow.  An all-zero column gives 0 - 0 = 0: an exact tie.
+              g1 = __ffma2_rn(make_float2(-cv, -cv), aa, make_float2(fabsf(vv.x), fabsf(vv.y)));
             } else {
+              // squared vote: sum k |k| against sum k^2 (error <= 11 * 2^-24 sum k^2 while k^2 is normal:
+              // the floor check below)
               vv = __fmul2_rn(k2[0], make_float2(fabsf(k2[0].x), fabsf(k2[0].y)));
-              gg = __fmul2_rn(k2[0], k2[0]);
+              float2 gg = __fmul2_rn(k2[0], k2[0]);
 #pragma unroll
               for (int i = 1; i < N; ++i) {
                 vv = __ffma2_rn(k2[i], make_float2(fabsf(k2[i].x), fabsf(k2[i].y)), vv);
                 gg = __ffma2_rn(k2[i], k2[i], gg);
               }
+              g1 = __ffma2_rn(make_float2(-cv, -cv), gg, make_float2(fabsf(vv.x), fabsf(vv.y)));
             }
-            // |vote| - c * bound (one rounding: its sign is exact).  < 0: the f32 vote's sign is not
-            // certain; an all-zero column gives 0 - 0 = 0 (an exact tie, no fallback needed)
-            g1 = __ffma2_rn(make_float2(-cv, -cv), gg, make_float2(fabsf(vv.x), fabsf(vv.y)));
             const float2 sg = make_float2(sign_one(vv.x), sign_one(vv.y));
             // t = k * sign(vote) + 0 (exact; +0 for k = 0): t < 0 <=> entry opposes the majority.
             // Erased entries are counted from t's sign bit; survivors enter as
@@ -991,6 +1074,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
               }
               y2 = __ffma2_rn(sg, acc, b2);
             }
+            // a finite vote and sum|k| do not rule out an overflow in y (sum k + sg sum|k| or t + |t|
+            // can exceed the f32 range): y * 0 + g1 is NaN exactly when y is inf or NaN, which the
+            // bracket below cannot see (a NaN y rounds both ends to the same word)
+            g1 = __ffma2_rn(y2, make_float2(0.f, 0.f), g1);
           } else {
             y2 = b2;
 #pragma unroll
@@ -1002,24 +1089,23 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
           // bf16 rounding must be certain.  The f32 evaluation error is <= (4 + N + 1) * 2^-24 * S with
           // S = |b| + max w * sum|k| (3 roundings in k, 1 in w, N in the weighted sum, 1 in y), so the
           // reference's value lies in [y - 2^-20 S, y + 2^-20 S] (the two bracket ends are rounded once
-          // each, losing at most 2^-25 S of the 16 * 2^-24 S margin: certified for N <= 10).  RN to bf16 is
+          // each, losing at most 2^-24 S of the 16 * 2^-24 S margin: certified for N <= 10).  RN to bf16 is
           // monotone, so if both ends round to the same bf16 word, so does the reference's value -- the
           // bracket covers the rounding boundaries on both sides of y, including the closer one below a
           // power of two.  The output IS the lower end's word.
-          const float2 S2 = __ffma2_rn(make_float2(wmax, wmax), aa, make_float2(fabsf(b2.x), fabsf(b2.y)));
           const float2 ylo = __ffma2_rn(make_float2(-0x1p-20f, -0x1p-20f), S2, y2);
           const float2 yhi = __ffma2_rn(make_float2(0x1p-20f, 0x1p-20f), S2, y2);
           const uint32_t wlo = pack_bf16x2(ylo);
           mx[p] = wlo ^ pack_bf16x2(yhi);
-          // The bounds above are relative (normal-range rounding).  They also hold when S >= 2^-90: a
-          // subnormal intermediate needs deltas below 2^-100, hence a base below 2^-93, hence S < 2^-90
-          // (squared vote: k^2 must stay normal, i.e. |k| >= 2^-63, which S >= 2^-38 guarantees with
-          // sr >= 2^-16).  g3 < 0 flags 0 < S < that floor (S == 0 is an all-zero column: exact);
-          // overflow to inf makes a margin NaN, which the NaN-propagating minimum turns into a fallback.
-          constexpr float kInvFloor = ERASE == 2 ? 0x1p38f : 0x1p90f;
-          // g3 = max(S / floor - 1, -S): < 0 exactly for 0 < S < floor (-0 for S == 0)
-          const float2 g3a = __ffma2_rn(S2, make_float2(kInvFloor, kInvFloor), make_float2(-1.f, -1.f));
-          gm[p] = fmin4_nan(g1.x, g1.y, fmaxf(g3a.x, -S2.x), fmaxf(g3a.y, -S2.y));
+          if constexpr (ERASE == 2) {
+            // unscaled squared vote: k^2 must stay normal (|k| >= 2^-63), which S >= 2^-38 guarantees
+            // with sr >= 2^-16; g3 = max(S * 2^38 - 1, -S) < 0 exactly for 0 < S < 2^-38 (-0 for S == 0,
+            // an all-zero column), and overflow to inf makes a margin NaN
+            const float2 g3a = __ffma2_rn(S2, make_float2(0x1p38f, 0x1p38f), make_float2(-1.f, -1.f));
+            gm[p] = fmin_nan(fmin3_nan(g1.x, g1.y, fmaxf(g3a.x, -S2.x)), fmaxf(g3a.y, -S2.y));
+          } else {
+            gm[p] = fmin_nan(g1.x, g1.y);
+          }
           outw[p] = wlo;
         }
         float gmin = gm[0];
@@ -1028,16 +1114,26 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         uint32_t anym = mx[0];
 #pragma unroll
         for (int q = 1; q < kFastPairs; ++q) anym |= mx[q];
-        uint32_t slowm = 0;
         if (!(gmin >= 0.f) || anym != 0u) {  // a margin negative or NaN, or a bracket straddling a boundary
+          uint32_t slowm = 0;
 #pragma unroll
           for (int q = 0; q < kFastPairs; ++q) {
             const uint32_t bad = !(gm[q] >= 0.f);
             slowm |= ((bad | ((mx[q] & 0xffffu) != 0u)) << (2 * q)) | ((bad | ((mx[q] >> 16) != 0u)) << (2 * q + 1));
           }
+          slowbits |= slowm << jit;
         }
-        slowbits |= slowm << jit;
         FastVec::store(outp + out_base + le, outw);
+      };
+      constexpr uint32_t kIters = ELEMS / (kFastElems * kFastCThreads);
+      static_assert(kIters * kFastElems * kFastCThreads == ELEMS, "a full stage is a whole number of iterations");
+      if (fast_ok && n == ELEMS) {
+        // full stage: compile-time trip count, constant smem / global offsets
+#pragma unroll
+        for (uint32_t it = 0; it < kIters; ++it) vec(tid + it * kFastCThreads, it * kFastElems);
+      } else if (fast_ok) {
+        uint32_t jit = 0;
+        for (uint32_t v = tid; v < nvec; v += kFastCThreads, jit += kFastElems) vec(v, jit);
       }
       // phase 2 (rare): exact reference-order evaluation of the recorded elements, read back from the
       // stage; the 2-byte store follows this thread's own vector store of the same word
@@ -1081,7 +1177,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 #pragma unroll
         for (int i = 0; i < N; ++i) cnt_er[i] += (erm >> i) & 1u;
         (void)nzm;
-        store_from_f64<RLK_BF16>(g.seg->out, idx, Y);
+        store_from_f64<RLK_BF16>(g.out, idx, Y);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&r.empty[s]);

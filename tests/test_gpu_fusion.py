@@ -388,13 +388,15 @@ def test_fast_path_power_of_two_boundaries(cuda):
 
 def test_fast_path_overflow_falls_back(cuda):
     """Deltas beyond the f32 range (|e - b| > 3.4e38) make the f32 merge produce inf, or NaN through a
-    zero weight times an infinite delta; with the erase vote off there is no vote margin to catch it,
-    so the fast path must still send those elements to the exact f64 path (the reference never
-    overflows in float64)."""
+    zero weight times an infinite delta, and finite deltas can still overflow the weighted sums; with
+    or without the erase vote the fast path must send those elements to the exact f64 path (the
+    reference never overflows in float64)."""
     from paper_2509_18883_b200 import fusion as F
     g = np.random.default_rng(8)
-    n = 1 << 16
-    base = bf16_round(g.choice([-1.0, 1.0], n) * 10.0 ** g.uniform(37.5, 38.4, n))
+    n = 1 << 18
+    # magnitudes from 1e29 (finite f32 deltas whose weighted sums overflow in the scaled fast path)
+    # to 2.5e38 (deltas beyond the f32 range)
+    base = bf16_round(g.choice([-1.0, 1.0], n) * 10.0 ** g.uniform(29.0, 38.4, n))
     experts = [bf16_round(-base * g.uniform(0.5, 1.0, n)), bf16_round(-base * 0.9), bf16_round(base * 0.5)]
     small = g.random(n) < 0.5  # half the columns stay in range
     for e in experts:
@@ -402,7 +404,9 @@ def test_fast_path_overflow_falls_back(cuda):
     bt = torch.from_numpy(base).to(cuda, torch.bfloat16)
     ets = [torch.from_numpy(e).to(cuda, torch.bfloat16) for e in experts]
     for cfgkw in (dict(target_norm=None, erase_mode=False, merge_weights=(1.0, 0.0, 0.0)),
-                  dict(target_norm=None, erase_mode=False, merge_weights=(0.5, 0.3, 0.2))):
+                  dict(target_norm=None, erase_mode=False, merge_weights=(0.5, 0.3, 0.2)),
+                  dict(target_norm=None), dict(target_norm=None, merge_weights=(0.5, 0.3, 0.2)),
+                  dict(target_norm=None, erase_weighting="squared"), dict(dropout_p=0.5, seed=3)):
         outs = []
         for exact in (False, True):
             o, _ = F.fuse_state_dict({"w": bt}, [{"w": e} for e in ets], F.FusionConfig(**cfgkw),
