@@ -529,7 +529,7 @@ def cpu_baseline(layout_name: str, p: float, cores: int | None = None, slice_ele
             "per_core": per_core, "cpu_seconds": cpu_s, "wall_s_incl_datagen": wall,
             "sample": f"oracle fuse (numpy f64, FusionConfig(dropout_p={p}, seed=42)) on layer 0 of {layout_name}: "
                       f"{params / 1e6:.1f}M params (first slices) in {len(jobs)} slices of <=4M elements, one process per core; "
-                      f"value = per-core rate (sum params / sum compute seconds) x cores"}
+                      f"value = per-core rate (sum params / sum compute seconds) x cores (extrapolated, ideal scaling)"}
 
 
 def _cpu_grpo_job(args):
@@ -561,7 +561,88 @@ def grpo_cpu_baseline(V: int = 131072, rows_per_job: int = 64, cores: int | None
     per_core = toks / cpu_s
     return {"value": per_core * cores, "unit": "tokens/s", "cores": cores, "kind": "port", "per_core": per_core,
             "sample": f"oracle token terms (numpy f64, V={V}) on {toks} synthetic rows, {rows_per_job} per process, "
-                      "one process per core; value = per-core rate x cores"}
+                      "one process per core; value = per-core rate x cores (extrapolated, ideal scaling)"}
+
+
+# ------------------------------------------------------------- the unmodified reference (rolloutlab)
+REF_DIR = ROOT / "baseline" / "_ref"  # `pip install --target baseline/_ref` of /root/reference/pkg (DESIGN 8)
+
+
+def _import_reference():
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    from rolloutlab import core, fusion, objective, toy_env  # noqa: F401
+    return core, fusion, objective, toy_env
+
+
+def _ref_fuse_job(args):
+    """rolloutlab.fusion.fuse, unmodified (its per-element Python dropout loop, fusion.py:105-115), on
+    one slice of a synthetic bf16-valued tensor."""
+    import numpy as np
+    _, fusion, _, toy_env = _import_reference()
+    t, n, p = args
+    g = np.random.default_rng([7, t])
+    b = g.normal(0, 0.02, n).astype(np.float32).astype(np.float64)
+    pt = lambda a: toy_env.ParamTable(a.reshape(1, 1, -1))
+    base = pt(b)
+    es = [pt(b + g.normal(0, 1e-3 * (i + 1), n)) for i in range(N_EXPERTS)]
+    t0 = time.perf_counter()
+    taus = [fusion.task_vector(e, base) for e in es]
+    fusion.fuse(base, taus, fusion.FusionConfig(dropout_p=p, seed=42))
+    return time.perf_counter() - t0, n
+
+
+def _ref_grpo_job(args):
+    """rolloutlab.objective.objective_value, unmodified, on one group of G responses over a V-wide
+    tabular policy (its per-token numpy log-softmax, toy_env.py:157-175)."""
+    import numpy as np
+    core, _, objective, toy_env = _import_reference()
+    seed, G, T, V = args
+    g = np.random.default_rng(seed)
+    # one context per response: every token reads its own logits row, as in config 5 (no cache reuse)
+    params = toy_env.ParamTable(g.normal(0, 2.0, (G, T, V)))
+    samples = []
+    for si in range(G):
+        toks = tuple(int(x) for x in g.integers(0, V, T))
+        lt = tuple(float(x) for x in g.normal(-12.0, 0.3, T))
+        li = tuple(x + 0.01 for x in lt)
+        rw = core.RewardOutcome.passed() if si % 2 == 0 else core.RewardOutcome.failed()
+        samples.append(core.Sample(prompt_id=0, context_id=si, version_id=0, tokens=toks, infer_logps=li,
+                                   status=core.SampleStatus.COMPLETE, t_start=0, train_logps=lt, reward=rw,
+                                   gen_temperature=1.0))
+    batch = objective.apply_masks([core.Group(0, tuple(samples))], T)
+    t0 = time.perf_counter()
+    objective.objective_value(batch, params, objective.ClipConfig())
+    return time.perf_counter() - t0, G * T
+
+
+def reference_cpu(p: float, cores: int | None = None, fuse_elems: int = 1 << 17, fuse_jobs_per_core: int = 2,
+                  grpo_g: int = 4, grpo_t: int = 32) -> dict:
+    """Times the UNMODIFIED reference (baseline/_ref) on a bounded sample, one process per core:
+    fusion = `fuse` on 131,072-element slices (3 experts, FusionConfig(dropout_p=p, seed=42));
+    GRPO = `objective_value` on one group of 4 x 32 tokens at V = 131,072.  Values are per-core rates x
+    cores (extrapolated to all cores, ideal scaling)."""
+    import concurrent.futures as cf
+    try:
+        _import_reference()
+    except Exception as e:  # not installed on this box
+        return {"unavailable": f"rolloutlab not importable from {REF_DIR}: {type(e).__name__}"}
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    cores = cores or os.cpu_count() or 1
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        fz = list(ex.map(_ref_fuse_job, [(k, fuse_elems, p) for k in range(cores * fuse_jobs_per_core)]))
+        gr = list(ex.map(_ref_grpo_job, [(k, grpo_g, grpo_t, 131072) for k in range(cores)]))
+    f_rate = sum(r[1] for r in fz) / sum(r[0] for r in fz)
+    g_rate = sum(r[1] for r in gr) / sum(r[0] for r in gr)
+    return {
+        "kind": "reference", "cores": cores,
+        "fusion": {"value": f_rate * cores, "unit": "params/s", "per_core": f_rate,
+                   "sample": f"rolloutlab.fusion.fuse unmodified, {len(fz)} slices x {fuse_elems} elements, 3 experts, "
+                             f"FusionConfig(dropout_p={p}, seed=42); value = per-core rate x {cores} cores (extrapolated)"},
+        "grpo": {"value": g_rate * cores, "unit": "tokens/s", "per_core": g_rate,
+                 "sample": f"rolloutlab.objective.objective_value unmodified, {len(gr)} groups of {grpo_g} x {grpo_t} "
+                           f"tokens, V=131072; value = per-core rate x {cores} cores (extrapolated)"},
+    }
 
 
 # ----------------------------------------------------------------------------------- main
@@ -612,17 +693,43 @@ def main():
             gc = grpo_cpu_baseline()
             line["grpo"] = {"workload": "config5 token terms, V=131072", "tokens_per_s": gc["value"],
                             "cpu_baseline": gc}
+        # the unmodified reference beside the port (the port is the line's value: it is ~15x faster
+        # than the reference's per-element Python dropout loop, so the ratio against it is conservative)
+        line["reference_unmodified"] = reference_cpu(args.dropout)
         print(json.dumps(line))
         return
 
     import torch
     fz = fusion_bench(args, rank, world, local, group)
     gr = None if args.no_grpo else grpo_bench(args, rank, world, local, group)
+    # BASELINE.json configs 2 and 1 (parity cases, reported beside the headline): the same step on the
+    # GPT-1.3B-shaped bf16 dict and on the 10M-param f32 MLP dict (L2 flushed between its steps)
+    others = {}
+    if world == 1 and not args.quick and args.layout == "llama8b":
+        for key, lay, dt in (("config2", "gpt1p3b", "bf16"), ("config1", "mlp10m", "f32")):
+            sub = argparse.Namespace(**{**vars(args), "layout": lay, "dtype": dt, "quick": True, "no_e2e": True})
+            r = fusion_bench(sub, rank, world, local, group)
+            es_ = {"bf16": 2, "f32": 4}[dt]
+            kb_ = {"rlk_fusion_sumsq": (N_EXPERTS + 1) * es_, "rlk_fusion_merge": (N_EXPERTS + 1) * es_ + es_}
+            kern_ = {k: v for k, v in r["kern_local"].items() if k in kb_}
+            dom_ = max(kern_, key=kern_.get)
+            ach_ = r["local_params"] * kb_[dom_] / (kern_[dom_] / 1e3) / 1e9
+            step_b = r["total_params"] * es_ * ((N_EXPERTS + 1) * 2 + 1)
+            others[key] = {"workload": f"{lay} {dt}, {r['total_params']} params, {r['n_tensors']} tensors, "
+                                       f"FusionConfig(dropout_p={args.dropout}, seed=42)",
+                           "value": r["total_params"] / (r["ms"] / 1e3), "unit": "params/s",
+                           "ms_per_step": r["ms"], "hbm_frac_step": step_b / (r["ms"] / 1e3) / 1e9 / peak,
+                           "roofline": {"bound": "hbm", "kernel": dom_, "achieved": ach_, "peak": peak,
+                                        "unit": "GB/s", "frac": ach_ / peak, "bytes_per_param": kb_[dom_],
+                                        "kernels_ms": r["kern_local"]},
+                           "l2": r["l2"], "launch": r["launch"], "clocks": r["clocks"]}
     cpu = gcpu = None
+    ref_cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.layout, args.dropout)
         if gr is not None:
             gcpu = grpo_cpu_baseline()
+        ref_cpu = reference_cpu(args.dropout)
     if rank != 0:
         if group is not None:
             import torch.distributed as dist
@@ -689,8 +796,12 @@ def main():
             line["grpo"]["variants"] = gr["variants"]
         if gcpu is not None:
             line["grpo"]["cpu_baseline"] = gcpu
+    if others:
+        line["other_configs"] = others
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if ref_cpu is not None:
+        line["cpu_baseline_reference_unmodified"] = ref_cpu
     print(json.dumps(line))
     if args.json_out:
         Path(args.json_out).write_text(json.dumps(line, indent=1))

@@ -215,8 +215,20 @@ def open_mmap(path) -> tuple[list[Entry], dict[str, np.memmap]]:
     return entries, maps
 
 
+def open_any(path) -> tuple[list[Entry], dict[str, np.memmap]]:
+    """Memory maps of a repo-format (RLKCKPT) or safetensors checkpoint (one file, a directory of
+    shards or an index.json: safetensors_io)."""
+    from . import safetensors_io as ST
+    if ST.is_safetensors(path):
+        return ST.open_mmap(path)
+    return open_mmap(path)
+
+
 def load(path, device=None, verify: bool = True) -> dict[str, torch.Tensor]:
     """Read a checkpoint onto the GPU; payload checksums verified on the device."""
+    from . import safetensors_io as ST
+    if ST.is_safetensors(path):
+        return ST.load(path, device, verify)
     entries, maps = open_mmap(path)
     dev = device or torch.device("cuda", torch.cuda.current_device())
     out = {}
@@ -273,14 +285,18 @@ def cmd_fuse(base_path, expert_paths: Sequence, out_path, cfg: FusionConfig = Fu
              device_budget_bytes: int = 32 << 30, on_unchanged: str = "passthrough") -> FuseReport:
     """Fuse checkpoint files: fused checkpoint + per-tensor FusionStats report.
 
+    Inputs may be repo-format checkpoints or safetensors (files, shard directories, index.json: see
+    safetensors_io); the output is safetensors when `out_path` ends in .safetensors, else repo format.
+
     Validation happens before the output is renamed into place: non-finite inputs raise
     ValueError("logits must be finite"); tensors no expert changed are written as the base and listed
     in `report.passthrough` (on_unchanged="raise": the reference's mean-norm ValueError instead)."""
+    from . import safetensors_io as ST
     from .loader import ArraySource, HostLoader, fuse_streaming
     if not expert_paths:
         raise ValueError("need at least one task vector")
-    base_e, base_m = open_mmap(base_path)
-    experts = [open_mmap(p) for p in expert_paths]
+    base_e, base_m = open_any(base_path)
+    experts = [open_any(p) for p in expert_paths]
     for ents, _ in experts:
         if [(e.name, e.shape, e.dtype) for e in ents] != [(e.name, e.shape, e.dtype) for e in base_e]:
             raise ValueError("shape mismatch between base and expert checkpoints")
@@ -288,8 +304,12 @@ def cmd_fuse(base_path, expert_paths: Sequence, out_path, cfg: FusionConfig = Fu
     if len(dtypes) != 1:
         raise ValueError("all tensors of a fused checkpoint must share one dtype")
     dt = DTYPES[dtypes.pop()][0]
-    entries, size = layout_entries([(e.name, e.dtype, e.shape) for e in base_e])
     out_path = Path(out_path)
+    st_out = out_path.suffix == ".safetensors"
+    if st_out:
+        st_head, entries, size = ST.layout([(e.name, e.dtype, e.shape) for e in base_e])
+    else:
+        entries, size = layout_entries([(e.name, e.dtype, e.shape) for e in base_e])
     tmp = out_path.with_name(out_path.name + ".tmp")
     try:
         with open(tmp, "wb") as f:
@@ -311,7 +331,7 @@ def cmd_fuse(base_path, expert_paths: Sequence, out_path, cfg: FusionConfig = Fu
         for e in entries:
             e.checksum = _u64(sink.sums[e.name])
         with open(tmp, "r+b") as f:
-            f.write(encode_header(entries))
+            f.write(ST.header_with_checksums(st_head, entries) if st_out else encode_header(entries))
             f.flush()
             os.fsync(f.fileno())
         os.replace(tmp, out_path)
