@@ -489,6 +489,123 @@ def grpo_bench(args, rank, world, local, group):
 
 
 # ----------------------------------------------------------------------------------- CPU baseline
+# ----------------------------------------------------------------------------- config 4 (streamed)
+def pcie_h2d_peak_gbs(dev, nbytes: int = 1 << 30, reps: int = 5) -> float:
+    """Bare pinned host -> device copy bandwidth on this rank's link (the streaming bound)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(dev)
+    with torch.cuda.stream(s):
+        d.copy_(h, non_blocking=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            d.copy_(h, non_blocking=True)
+        e1.record(s)
+    torch.cuda.synchronize(dev)
+    return nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
+class PinnedPoolSource:
+    """A checkpoint already resident in page-locked host memory: every (tensor, stream) is a slice of
+    one pinned pool of synthetic bf16 values at a hashed offset, DMA'd directly (the loader's pinned
+    path).  Host-side synthesis (loader.SyntheticSource) runs at ~1 GB/s on this host, far below the
+    link, so it would measure the CPU, not the streaming path."""
+
+    def __init__(self, pool_elems: int = 1 << 31, seed: int = 0):
+        import numpy as np
+        import torch
+        g = np.random.default_rng(seed)
+        vals = (g.standard_normal(pool_elems // 16, dtype=np.float32) * 0.02).view(np.uint32) >> 16
+        self.pool = torch.from_numpy(np.tile(vals.astype(np.uint16).view(np.int16), 16)).pin_memory()
+        self.n = pool_elems
+
+    def fill(self, loader, name, si, dst, stream):
+        import zlib
+        n = dst.numel()
+        off = (zlib.crc32(f"{name}/{si}".encode()) * 4099) % max(1, self.n - n) & ~63
+        loader.h2d(dst, self.pool[off:off + n].numpy(), stream)
+
+
+def stream_bench(args, rank, world, local, group, peak, peak_src) -> dict | None:
+    """BASELINE.json configs[3]: LongCat-Flash-560B-MoE-shaped random-init experts (layouts.longcat_560b,
+    `--stream-layers` of its 28 layers + embeddings/head), fused by streaming tensor groups through
+    pinned host buffers (K7).  Host workers synthesise base + 3 experts (counter hash) straight into
+    pinned slots; outputs are checksummed on the way back (larger than RAM).  Under torchrun every
+    rank streams its whole-tensor share (`loader.partition_tensors`) over its own PCIe link: no
+    parameter data or norm crosses GPUs.  A step = one complete streamed fusion of the slice."""
+    import torch
+    from paper_2509_18883_b200 import fusion as F
+    from paper_2509_18883_b200.layouts import longcat_560b, numel
+    from paper_2509_18883_b200.loader import (ChecksumSink, HostLoader, SyntheticSource, fuse_streaming,
+                                              partition_tensors)
+    dev = torch.device("cuda", local)
+    shapes = longcat_560b(n_layers=args.stream_layers)
+    names = list(shapes)
+    numels = [numel(s) for s in shapes.values()]
+    total = sum(numels)
+    full = sum(numel(s) for s in longcat_560b().values())
+    mine = sum(numels[t] for t in partition_tensors(numels, world, rank))
+    pcie = pcie_h2d_peak_gbs(dev)
+    cfg = F.FusionConfig(dropout_p=args.dropout, seed=42)
+    ld = HostLoader(slot_bytes=64 << 20, n_slots=6)
+    src = SyntheticSource() if args.stream_source == "synth" else PinnedPoolSource()
+    sink = ChecksumSink()
+
+    def step():
+        return fuse_streaming(names, numels, N_EXPERTS, src, sink, cfg, device_budget_bytes=48 << 30, stats=False,
+                              loader=ld, world=world, rank=rank)
+
+    for _ in range(args.warmup):
+        step()
+    times, reps = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            barrier(group)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            reps.append(step())  # returns after its final device synchronize
+            times.append(time.perf_counter() - t0)
+    ld.close()
+    sec = statistics.mean(times)
+    h2d = reps[-1].h2d_bytes
+    h2d_gbs = h2d / sec / 1e9
+    sec_max, = max_over_ranks([sec], group)
+    per_rank = [0.0] * world
+    vals = torch.zeros(world, 3, dtype=torch.float64, device=dev)
+    vals[rank] = torch.tensor([h2d_gbs, pcie, mine], dtype=torch.float64)
+    if group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(vals, group=group)
+    per_rank = vals.cpu().tolist()
+    if rank != 0:
+        return None
+    alg = total * (2 * (N_EXPERTS + 1) * 2 + 2)  # 18 B/param of HBM traffic (SURVEY 8(d))
+    return {
+        "metric": METRIC, "value": total / sec_max, "unit": "params/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec_max * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init bf16 values in host memory)",
+        "config": {"workload": f"config4: LongCat-Flash-560B-MoE-shaped bf16 (layouts.longcat_560b, "
+                               f"{args.stream_layers} of 28 layers + embeddings/head: {total} params, {len(numels)} "
+                               f"tensors; full model {full}), 3 experts + base, FusionConfig(dropout_p={args.dropout}, "
+                               f"seed=42), streamed from host ({'host-synthesised' if args.stream_source == 'synth' else 'pinned pool'} "
+                               f"source, checksum sink), whole-tensor shards x{world}",
+                   "timing": "wall clock around each complete streamed step (host synthesis, H2D, kernels, D2H "
+                             "and the final device synchronize), max over ranks"},
+        "stream": {"h2d_bytes_per_step_rank0": h2d, "h2d_gbs_per_rank": [r[0] for r in per_rank],
+                   "pcie_h2d_peak_gbs_per_rank": [r[1] for r in per_rank],
+                   "h2d_frac_of_pcie_peak": [r[0] / r[1] for r in per_rank],
+                   "params_per_rank": [int(r[2]) for r in per_rank],
+                   "hbm_gbs": alg / sec_max / 1e9, "hbm_frac": alg / sec_max / 1e9 / peak,
+                   "hbm_peak": peak, "hbm_peak_source": peak_src,
+                   "projected_full_model_s": full / (total / sec_max)},
+        "clocks": clk.summary(),
+        "e2e": {"value": total / sec_max, "unit": "params/s", "h2d_bytes_per_step": int(total * 2 * (N_EXPERTS + 1)),
+                "d2h_bytes_per_step": int(total * 2)},
+    }
+
+
 def _cpu_job(args):
     """One oracle fuse over a slice of a synthetic bf16-valued tensor (f64 math, like the reference)."""
     import numpy as np
@@ -664,6 +781,10 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the timed fusion steps eagerly")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--stream", action="store_true",
+                    help="config 4: stream --layout longcat560b from host memory (K7) instead of the in-HBM step")
+    ap.add_argument("--stream-layers", type=int, default=1, help="layers of the 28-layer longcat560b layout")
+    ap.add_argument("--stream-source", choices=["pinned", "synth"], default="pinned")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local, group = dist_setup(args)
@@ -700,6 +821,16 @@ def main():
         return
 
     import torch
+    if args.stream:
+        line = stream_bench(args, rank, world, local, group, peak, peak_src)
+        if line is not None:
+            print(json.dumps(line))
+            if args.json_out:
+                Path(args.json_out).write_text(json.dumps(line, indent=1))
+        if group is not None:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     fz = fusion_bench(args, rank, world, local, group)
     gr = None if args.no_grpo else grpo_bench(args, rank, world, local, group)
     # BASELINE.json configs 2 and 1 (parity cases, reported beside the headline): the same step on the

@@ -138,6 +138,9 @@ class StreamingReport:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     passthrough: list = field(default_factory=list)  # tensors no expert changed (written as the base)
+    tensors: int = 0  # tensors this rank streamed
+    params: int = 0
+    error: str | None = None  # a sharded rank's validation failure, raised after the gather
 
 
 def plan_groups(numels: Sequence[int], n_experts: int, esize: int, budget_bytes: int) -> list[list[int]]:
@@ -180,11 +183,30 @@ def _footprint(n: int, n_experts: int, esize: int) -> int:
     return (n + 63) // 64 * 64 * esize * (n_experts + 2)
 
 
+def partition_tensors(numels: Sequence[int], world: int, rank: int) -> list[int]:
+    """Rank `rank`'s tensors for streamed fusion: contiguous runs of whole tensors balanced by element
+    count (a cut falls at the first tensor boundary at or after k/world of the elements).  Norms are
+    per tensor, so whole-tensor shards need no collective at all (config 4)."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    total = sum(numels)
+    cuts, acc, t = [0], 0, 0
+    for r in range(1, world):
+        target = total * r / world
+        while t < len(numels) and acc + numels[t] / 2 < target:  # cut nearest the target
+            acc += numels[t]
+            t += 1
+        cuts.append(max(t, cuts[-1]))
+    cuts.append(len(numels))
+    return list(range(cuts[rank], cuts[rank + 1]))
+
+
 def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, source, sink,
                    cfg: FusionConfig = FusionConfig(), dtype: torch.dtype = torch.bfloat16,
                    device_budget_bytes: int = 64 << 30, stats: bool = True,
                    loader: HostLoader | None = None, group_bytes: int = 2 << 30,
-                   on_unchanged: str = "passthrough") -> StreamingReport:
+                   on_unchanged: str = "passthrough", world: int = 1, rank: int = 0,
+                   group=None, _defer_errors: bool = False) -> StreamingReport:
     """Fuse a host-resident (or synthesised) checkpoint through the device in pipelined groups.
 
     Consecutive tensors are grouped up to min(`group_bytes`, half the budget) of device footprint
@@ -198,9 +220,38 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
 
     After the last group: non-finite inputs raise ValueError("logits must be finite"); tensors no
     expert changed are listed in `report.passthrough` (written as the base), or raise the reference's
-    "cannot take mean norm of all-zero task vectors" with on_unchanged="raise"."""
+    "cannot take mean norm of all-zero task vectors" with on_unchanged="raise".
+
+    Multi-GPU (one process per GPU): with `world` > 1 this rank streams only its whole-tensor share
+    (`partition_tensors`) -- every rank reads its own slice of the checkpoint over its own PCIe link and
+    no parameter data or norm crosses GPUs.  With a process group the per-tensor statistics (and the
+    validation outcome) are gathered so every rank returns the full report."""
     if on_unchanged not in ("passthrough", "raise"):
         raise ValueError("on_unchanged must be 'passthrough' or 'raise'")
+    if group is not None:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if world > 1:
+        mine = partition_tensors(numels, world, rank)
+        rep = fuse_streaming([names[t] for t in mine], [numels[t] for t in mine], n_experts, source, sink, cfg,
+                             dtype, device_budget_bytes, stats, loader, group_bytes, "passthrough",
+                             _defer_errors=True) if mine else StreamingReport()
+        rep.tensors = len(mine)
+        rep.params = sum(numels[t] for t in mine)
+        if group is not None:
+            import torch.distributed as dist
+            parts = [None] * world
+            dist.all_gather_object(parts, (rep.stats, rep.passthrough, rep.error), group=group)
+            errs = [e for _, _, e in parts if e]
+            if errs:
+                raise ValueError(errs[0])
+            rep.stats = {k: v for st, _, _ in parts for k, v in st.items()}
+            rep.passthrough = [n for _, pt, _ in parts for n in pt]
+        elif rep.error:
+            raise ValueError(rep.error)
+        if rep.passthrough and on_unchanged == "raise":
+            raise ValueError("cannot take mean norm of all-zero task vectors")
+        return rep
     dev = torch.device("cuda", torch.cuda.current_device())
     esize = torch.tensor([], dtype=dtype).element_size()
     cap = device_budget_bytes // esize // 64 * 64  # ring capacity in elements
@@ -295,8 +346,12 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
                 elif st == 1:
                     unchanged.append(names[t])
         if bad:
-            raise ValueError(f"logits must be finite (non-finite values in {bad[:8]}"
-                             f"{' ...' if len(bad) > 8 else ''})")
+            msg = (f"logits must be finite (non-finite values in {bad[:8]}"
+                   f"{' ...' if len(bad) > 8 else ''})")
+            if _defer_errors:  # a sharded caller reports it after every rank is done (no rank left hanging)
+                rep.error = msg
+            else:
+                raise ValueError(msg)
         if unchanged and on_unchanged == "raise":
             raise ValueError("cannot take mean norm of all-zero task vectors")
         rep.passthrough = unchanged

@@ -121,3 +121,38 @@ def grpo_worker(rank: int, world: int, port: int, backend: str):
         raise
     finally:
         dist.destroy_process_group()
+
+
+def stream_worker(rank: int, world: int, port: int, backend: str):
+    """fuse_streaming(group=...): each rank streams its tensors; the gathered statistics on every rank
+    equal the all-in-HBM fuse's, and each rank's outputs match it bit for bit."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2509_18883_b200 import fusion as F
+    from paper_2509_18883_b200.loader import ArraySink, ArraySource, fuse_streaming, partition_tensors
+    from tests.helpers import bf16_round, synth_state_dicts
+    dev, group = _init(rank, world, port, backend)
+    try:
+        shapes = {f"t{i}": (100 + 37 * i, 65) for i in range(9)}
+        base, experts = synth_state_dicts(shapes, 3, seed=5, dtype_round=bf16_round)
+        hb = {k: torch.from_numpy(v.astype(np.float32)).to(torch.bfloat16) for k, v in base.items()}
+        he = [{k: torch.from_numpy(v.astype(np.float32)).to(torch.bfloat16) for k, v in e.items()} for e in experts]
+        names = list(hb)
+        out = {k: torch.zeros(v.shape, dtype=torch.bfloat16) for k, v in hb.items()}
+        cfg = F.FusionConfig(dropout_p=0.5, seed=2)
+        rep = fuse_streaming(names, [hb[k].numel() for k in names], 3, ArraySource(hb, he), ArraySink(out), cfg,
+                             device_budget_bytes=4 << 20, group=group)
+        ref, rrep = F.fuse_state_dict({k: v.to(dev) for k, v in hb.items()},
+                                      [{k: v.to(dev) for k, v in e.items()} for e in he], cfg)
+        assert sorted(rep.stats) == sorted(names)
+        for k in names:
+            assert rep.stats[k] == rrep.stats(k), (rank, k)
+        for t in partition_tensors([hb[k].numel() for k in names], world, rank):
+            k = names[t]
+            assert torch.equal(out[k].view(torch.int16), ref[k].cpu().view(torch.int16)), (rank, k)
+    except Exception:
+        traceback.print_exc()
+        raise
+    finally:
+        dist.destroy_process_group()

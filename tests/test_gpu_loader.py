@@ -129,3 +129,32 @@ def test_streaming_validates_inputs(cuda, tmp_path):
     with pytest.raises(ValueError, match="logits must be finite"):
         CK.cmd_fuse(paths[0], paths[1:], dst, F.FusionConfig())
     assert not dst.exists() and not (tmp_path / "fused.rlk.tmp").exists()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_partitioned_stream_equals_in_hbm(cuda, world):
+    """Config-4 sharding: every rank streams its whole-tensor share (`partition_tensors`); the union of
+    the ranks' outputs and statistics equals the all-in-HBM fuse bit for bit (norms are per tensor, so
+    no collective is involved).  Ranks run one after another on this GPU."""
+    from paper_2509_18883_b200 import fusion as F
+    from paper_2509_18883_b200.loader import ArraySink, ArraySource, fuse_streaming, partition_tensors
+    base, experts = synth_state_dicts(SHAPES, 3, seed=9, dtype_round=bf16_round)
+    hb, he = _host_bf16(base), [_host_bf16(e) for e in experts]
+    names = list(hb)
+    numels = [hb[k].numel() for k in names]
+    cfg = F.FusionConfig(dropout_p=0.5, seed=11)
+    out = {k: torch.zeros(v.shape, dtype=torch.bfloat16) for k, v in hb.items()}
+    stats, seen = {}, []
+    for r in range(world):
+        rep = fuse_streaming(names, numels, 3, ArraySource(hb, he), ArraySink(out), cfg, device_budget_bytes=16 << 20,
+                             world=world, rank=r)
+        mine = [names[t] for t in partition_tensors(numels, world, r)]
+        assert sorted(rep.stats) == sorted(mine) and rep.tensors == len(mine)
+        stats.update(rep.stats)
+        seen += mine
+    assert sorted(seen) == sorted(names)
+    dev_out, drep = F.fuse_state_dict({k: v.to(cuda) for k, v in hb.items()},
+                                      [{k: v.to(cuda) for k, v in e.items()} for e in he], cfg)
+    for k in names:
+        assert torch.equal(out[k].view(torch.int16), dev_out[k].cpu().view(torch.int16)), k
+        assert stats[k] == drep.stats(k)

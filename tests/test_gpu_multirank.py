@@ -29,3 +29,7 @@ def test_sharded_fusion_multirank(cuda, world, cfgkw):
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_grpo_multirank(cuda, world):
     mp.spawn(W.grpo_worker, args=(world, _port(), "gloo"), nprocs=world, join=True)
+
+
+def test_streamed_fusion_multirank(cuda):
+    mp.spawn(W.stream_worker, args=(2, _port(), "gloo"), nprocs=2, join=True)
