@@ -259,102 +259,51 @@ def fusion_bench(args, rank, world, local, group):
             res["variants"][vname] = ms0
             del call0
 
-    # e2e through the public API with pinned host buffers
-    if not args.no_e2e:
-        res.update(fusion_e2e(args, pieces, call, weights, stream, dev, group))
+    cfg_run = call.cfg
     del call, pieces
     torch.cuda.empty_cache()
+    # e2e through the public API with pinned host buffers
+    if not args.no_e2e:
+        res.update(fusion_e2e(args, layout, cfg_run, stream, dev, rank, world, group))
+        torch.cuda.empty_cache()
     return res
 
 
-def fusion_e2e(args, pieces, call, weights, stream, dev, group):
-    """End to end through the public API from pinned host memory, every step: H2D of base + experts,
-    fusion, D2H of the fused output.  At N = 1 the state dict is processed in tensor groups on three
-    streams -- H2D of group g+1, K2/K1/finalize/K3 of group g and D2H of group g-1 overlap (per-tensor
-    norms only need the tensor's own data).  At N > 1 the sharded step runs after a full H2D."""
+def fusion_e2e(args, layout, cfg, stream, dev, rank, world, group):
+    """End to end through the public API (loader.fuse_streaming) from pinned host memory, every step:
+    H2D of base + experts, fusion, D2H of the fused output, in tensor groups on three streams -- H2D of
+    group g+1, K2/K1/finalize/K3 of group g and D2H of group g-1 overlap (per-tensor norms only need the
+    tensor's own data).  Under torchrun every rank streams its whole-tensor share
+    (`loader.partition_tensors`) over its own link: no parameter data or norm crosses GPUs."""
     import torch
-    from paper_2509_18883_b200 import fusion as F
-    total = sum(p.numel for p in pieces)
-    dt = pieces[0].base.dtype
-    host_in = [torch.empty(total, dtype=dt, pin_memory=True) for _ in range(N_EXPERTS + 1)]
-    host_out = torch.empty(total, dtype=dt, pin_memory=True)
-    views = []
-    off = 0
-    for p in pieces:
-        n = p.numel
-        views.append((p, [h[off:off + n] for h in host_in], host_out[off:off + n]))
-        off += n
+    from paper_2509_18883_b200.layouts import fill_synthetic
+    from paper_2509_18883_b200.loader import ArraySink, ArraySource, fuse_streaming, partition_tensors
+    dt = {"bf16": torch.bfloat16, "f32": torch.float32}[args.dtype]
+    numels = list(layout.numels)
+    names = [str(t) for t in range(len(numels))]
+    mine = partition_tensors(numels, world, rank)
+    hb, he, ho = {}, [dict() for _ in range(N_EXPERTS)], {}
     with torch.cuda.stream(stream):
-        for p, hv, _ in views:
-            for h, d in zip(hv, [p.base, *p.experts]):
-                h.copy_(d, non_blocking=True)
-    stream.synchronize()
-    world = 1 if group is None else torch.distributed.get_world_size(group)
-    pipelined = world == 1
-    api = pipelined and os.environ.get("RLK_E2E_MANUAL", "0") != "1"
-    if api:
-        # the public streaming API (loader.fuse_streaming): pinned host dicts in, pinned host dict out
-        from paper_2509_18883_b200.loader import ArraySink, ArraySource, fuse_streaming
-        names = [str(k) for k in range(len(views))]
-        api_b = {n: v[1][0] for n, v in zip(names, views)}
-        api_e = [{n: v[1][i + 1] for n, v in zip(names, views)} for i in range(N_EXPERTS)]
-        api_o = {n: v[2] for n, v in zip(names, views)}
-        numels = [v[0].numel for v in views]
-    elif pipelined:
-        # consecutive tensor groups of ~2 GB of inputs; one FusionCall (plan) per group
-        groups, cur, cur_b = [], [], 0
-        for v in views:
-            cur.append(v)
-            cur_b += v[0].numel * 2 * (N_EXPERTS + 1)
-            if cur_b >= (2 << 30):
-                groups.append(cur)
-                cur, cur_b = [], 0
-        if cur:
-            groups.append(cur)
-        h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        calls = []
-        for gv in groups:
-            gp = [F.Piece(k, 0, v[0].base, v[0].experts, v[0].out) for k, v in enumerate(gv)]
-            calls.append(F.FusionCall(gp, F.FusionLayout([v[0].numel for v in gv]), N_EXPERTS, call.cfg, stream=stream))
+        for t in mine:  # the same synthetic values as the in-HBM step, generated on the device, pinned on the host
+            n = numels[t]
+            b = torch.empty(n, dtype=dt, device=dev)
+            es = [torch.empty(n, dtype=dt, device=dev) for _ in range(N_EXPERTS)]
+            fill_synthetic(b, es, t, j0=0, seed=0, stream=stream)
+            hb[names[t]] = torch.empty(n, dtype=dt, pin_memory=True)
+            hb[names[t]].copy_(b, non_blocking=True)
+            for i in range(N_EXPERTS):
+                he[i][names[t]] = torch.empty(n, dtype=dt, pin_memory=True)
+                he[i][names[t]].copy_(es[i], non_blocking=True)
+            ho[names[t]] = torch.empty(n, dtype=dt, pin_memory=True)
+            stream.synchronize()
+            del b, es
+    mine_params = sum(numels[t] for t in mine)
 
     def step():
-        if api:
-            with torch.cuda.stream(stream):
-                fuse_streaming(names, numels, N_EXPERTS, ArraySource(api_b, api_e), ArraySink(api_o), call.cfg,
-                               dtype=dt, device_budget_bytes=int(args.e2e_budget_gb * (1 << 30)), group_bytes=2 << 30)
-            return
-        if not pipelined:
-            with torch.cuda.stream(stream):
-                for p, hv, _ in views:
-                    for h, d in zip(hv, [p.base, *p.experts]):
-                        d.copy_(h, non_blocking=True)
-                call.run(weights)
-                for p, _, ho in views:
-                    ho.copy_(p.out, non_blocking=True)
-            return
-        # the compute stream is the one the timing events are recorded on: make it wait for the tail
-        start = torch.cuda.Event()
-        start.record(stream)
-        h2d_s.wait_event(start)
-        d2h_s.wait_event(start)
-        for gv, c in zip(groups, calls):
-            with torch.cuda.stream(h2d_s):
-                for p, hv, _ in gv:
-                    for h, d in zip(hv, [p.base, *p.experts]):
-                        d.copy_(h, non_blocking=True)
-            ready = torch.cuda.Event()
-            ready.record(h2d_s)
-            stream.wait_event(ready)
-            c.run(weights)
-            done = torch.cuda.Event()
-            done.record(stream)
-            d2h_s.wait_event(done)
-            with torch.cuda.stream(d2h_s):
-                for p, _, ho in gv:
-                    ho.copy_(p.out, non_blocking=True)
-        end = torch.cuda.Event()
-        end.record(d2h_s)
-        stream.wait_event(end)
+        with torch.cuda.stream(stream):
+            fuse_streaming(names, numels, N_EXPERTS, ArraySource(hb, he), ArraySink(ho), cfg, dtype=dt,
+                           device_budget_bytes=int(args.e2e_budget_gb * (1 << 30)), group_bytes=2 << 30,
+                           world=world, rank=rank)
 
     steps, warm = max(1, min(args.steps, args.e2e_steps)), 1
     for _ in range(warm):
@@ -369,13 +318,13 @@ def fusion_e2e(args, pieces, call, weights, stream, dev, group):
     torch.cuda.synchronize(dev)
     barrier(group)
     ms, = max_over_ranks([e0.elapsed_time(e1) / steps], group)
-    h2d, d2h = sum_over_ranks([float(total * 2 * (N_EXPERTS + 1)), float(total * 2)], group)
-    del host_in, host_out, views
+    es_ = dt.itemsize
+    h2d, d2h = sum_over_ranks([float(mine_params * es_ * (N_EXPERTS + 1)), float(mine_params * es_)], group)
+    del hb, he, ho
     return dict(e2e_ms=ms, e2e_steps=steps, e2e_warmup=warm, h2d=int(h2d), d2h=int(d2h),
                 e2e_path=("loader.fuse_streaming (public API): pinned host dicts, 2 GiB tensor groups, "
-                          "H2D | fuse | D2H on 3 streams, FusionStats returned" if api else
-                          "pipelined tensor groups (H2D | fuse | D2H on 3 streams)" if pipelined
-                          else "sharded: H2D, fuse with NCCL norm all_reduce, D2H"))
+                          "H2D | fuse | D2H on 3 streams, FusionStats returned"
+                          + (f"; whole-tensor shards x{world}, one PCIe link per rank" if world > 1 else "")))
 
 
 # ----------------------------------------------------------------------------------- GRPO

@@ -4,9 +4,10 @@ Fusion shards by parameter range: the global item list (every tensor cut into RL
 items from its own start) is split into world-size contiguous ranges balanced by element count
 (`FusionLayout.partition`).  Each rank holds only its range of base + experts and writes only its
 range of the output.  The one exchange is the all_reduce of the f64 norm partials between K1 and
-finalize -- every (item, expert) slot is produced by exactly one rank and is exactly zero elsewhere,
-so the NCCL sum is exact and the norms (hence scales, masks, erase decisions and outputs) are
-bit-identical at every world size.  With `FusionLayout.partition_striped` (the default here) the
+finalize, restricted to the item rows of the tensors that are split over ranks (a tensor held whole by
+one rank needs no exchange) -- every (item, expert) slot is produced by exactly one rank and is
+exactly zero elsewhere, so the NCCL sum is exact and the norms (hence scales, masks, erase decisions
+and outputs) are bit-identical at every world size.  With `FusionLayout.partition_striped` (the default here) the
 embedding-sized tensors are cut into one stripe per rank, so each rank draws only the dropout keep
 bits of its own index ranges and no bitmap crosses GPUs.  FusionStats counters are summed by a second (int64) all_reduce
 only when statistics are requested.
@@ -87,11 +88,18 @@ class ShardedFusion:
         return self
 
     def stats(self) -> dict[str, FusionStats]:
-        """Global FusionStats per tensor (sums this rank's counters with the others')."""
-        counters = allreduce_counts(self.call.counters.clone(), self.group)
-        saved = self.call.counters
-        self.call.counters = counters
+        """Global FusionStats per tensor: counters summed over ranks; each tensor's sum of squares and
+        scale from its owner rank (the only one contributing a non-zero row: exact sums)."""
+        c = self.call
+        counters = allreduce_counts(c.counters.clone(), self.group)
+        sumsq, scale = c.sumsq, c.scale
+        if c._owner is not None:
+            own = c._owner.view(-1, 1)
+            sumsq = allreduce_partials(torch.where(own, c.sumsq, torch.zeros_like(c.sumsq)), self.group)
+            scale = allreduce_partials(torch.where(own, c.scale, torch.zeros_like(c.scale)), self.group)
+        saved = c.counters, c.sumsq, c.scale
+        c.counters, c.sumsq, c.scale = counters, sumsq, scale
         try:
-            return {n: self.call.stats(t, self.weights) for t, n in enumerate(self.names)}
+            return {n: c.stats(t, self.weights) for t, n in enumerate(self.names)}
         finally:
-            self.call.counters = saved
+            c.counters, c.sumsq, c.scale = saved

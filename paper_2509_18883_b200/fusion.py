@@ -292,6 +292,12 @@ class FusionCall:
         self.bitmap = None
         self.words_per_row = 0
         self.timers: dict[str, list] | None = None  # name -> [(start_event, end_event)] when profiling
+        # sharded norms: tensors this rank holds pieces of, and (set on the first sharded step) the item
+        # rows of the tensors split over ranks -- the only partials that are exchanged -- plus each
+        # tensor's owner rank (the lowest holding it), which contributes its row to gathered statistics
+        self.held = sorted({p.tensor for p in pieces})
+        self._shared_rows: torch.Tensor | None = None
+        self._owner: torch.Tensor | None = None
 
     def _launch(self, name: str, *args) -> None:
         if self.timers is None:
@@ -366,17 +372,26 @@ class FusionCall:
                 world = dist.get_world_size(self.group)
             if self.partials is None or self.partials.numel() != self.layout.n_items * self.n:
                 self.partials = torch.zeros(self.layout.n_items * self.n, dtype=torch.float64, device=self.device)
-            elif world > 1:
-                self.partials.zero_()  # other ranks' slots must be exactly zero for the exact sum
+            if world > 1:
+                if self._shared_rows is None:
+                    self._shared_plan(world)
+                if self._shared_rows.numel():
+                    # other ranks' slots of the split tensors must be exactly zero for the exact sum
+                    self.partials.view(-1, self.n).index_fill_(0, self._shared_rows, 0.0)
             self._bitmap(s)
             seeds = (L.C.c_uint64 * self.n)(*self.seeds)
             self._launch("rlk_fusion_sumsq", L.C.byref(self.plan.c), self.n, L.dtype_code(self.dtype_in),
                          int(self.delta_mode), L.ptr(self.partials), L.ptr(self.counters), self.dropout_mode,
                          seeds, self.thresh, L.ptr(self.bitmap), self.words_per_row, s)
-            if self.group is not None:
-                # disjoint slots: the sum is exact, so norms are identical at every world size
+            if world > 1 and self._shared_rows.numel():
+                # only the item rows of tensors split over ranks cross GPUs (a tensor held by one rank
+                # has all its partials there already); every row has exactly one non-zero contributor,
+                # so the sum is exact and the norms are identical at every world size
                 from .dist import allreduce_partials
-                allreduce_partials(self.partials, self.group)
+                rows = self.partials.view(-1, self.n)
+                buf = rows.index_select(0, self._shared_rows)
+                allreduce_partials(buf, self.group)
+                rows.index_copy_(0, self._shared_rows, buf)
             self._launch("rlk_fusion_finalize", L.ptr(self.partials),
                          L.ptr(self.layout.tensor_items_device(self.device, self.stream)), self.layout.n_tensors,
                          self.n, self.cfg.target_mode,
@@ -384,8 +399,31 @@ class FusionCall:
                          L.ptr(self.sumsq), L.ptr(self.scale), L.ptr(self.status), s)
         return self
 
+    def _shared_plan(self, world: int) -> None:
+        """Once per sharded call: which tensors are split over ranks (their item rows are the partials
+        that get all-reduced) and which rank owns each tensor's statistics (two tiny all_reduces)."""
+        import torch.distributed as dist
+        nt = self.layout.n_tensors
+        held = torch.zeros(nt, dtype=torch.int64, device=self.device)
+        held[self.held] = 1
+        cnt = held.clone()
+        dist.all_reduce(cnt, group=self.group)
+        rank = dist.get_rank(self.group)
+        owner = torch.where(held > 0, torch.full_like(held, rank), torch.full_like(held, world))
+        dist.all_reduce(owner, op=dist.ReduceOp.MIN, group=self.group)
+        ti = self.layout.tensor_items
+        shared = [t for t in (cnt >= 2).nonzero().flatten().tolist()]
+        rows = np.concatenate([np.arange(ti[t], ti[t + 1], dtype=np.int64) for t in shared]) if shared \
+            else np.zeros(0, dtype=np.int64)
+        self._shared_rows = torch.from_numpy(rows).to(self.device)
+        self._owner = owner == rank
+
     def check_status(self, per_tensor_raise: bool = True) -> torch.Tensor:
         st = self.status.cpu()
+        if self._owner is not None:  # sharded: only the tensors this rank holds were normalised here
+            mask = torch.zeros_like(st, dtype=torch.bool)
+            mask[self.held] = True
+            st = torch.where(mask, st, torch.zeros_like(st))
         if per_tensor_raise:
             if bool((st == 2).any()):
                 raise ValueError("logits must be finite")
