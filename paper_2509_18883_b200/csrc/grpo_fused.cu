@@ -98,32 +98,49 @@ __device__ __forceinline__ void unpack8(const uint4 w, float* z) {
   z[4] = bf16_lo(w.z); z[5] = bf16_hi(w.z); z[6] = bf16_lo(w.w); z[7] = bf16_hi(w.w);
 }
 
-// Pass 1 over one chunk of a half row: online max / sum of 2^(z c - m c) in (mz, s[4]); nb = -mz c.
-// Two 16-byte vectors per thread per step (a full chunk is exactly two): one max test per 16 logits.
+// max of the bf16 pairs of two words, per half (max.bf16x2: HMNMX2.BF16, no unpacking)
+__device__ __forceinline__ uint32_t hmax2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ float2 bf16x2_f32(uint32_t w) { return make_float2(bf16_lo(w), bf16_hi(w)); }
+
+// Pass 1 over one chunk of a half row: online max / sum of 2^(z c - m c) in (mz, s[2] pairs); nb = -mz c.
+// Two 16-byte vectors per thread per step (a full chunk is exactly two): one max test per 16 logits,
+// the max taken on the packed bf16 words, the exponent arguments and sums in f32x2 (FFMA2 / FADD2).
 struct RowAcc {
-  float mz, s[4], nb;
+  float mz, nb;
+  float2 s[2];
   __device__ void reset() {
     mz = -INFINITY;
-    s[0] = s[1] = s[2] = s[3] = 0.f;
+    s[0] = s[1] = make_float2(0.f, 0.f);
     nb = INFINITY;
   }
   template <int NV>
   __device__ __forceinline__ void step(const uint8_t* cb, uint32_t v, float c) {
-    float z[8 * NV];
+    uint32_t w[4 * NV];
 #pragma unroll
-    for (int u = 0; u < NV; ++u) unpack8(lds128(cb + (v + u * kFT) * 16), z + 8 * u);
-    float lm = z[0];
+    for (int u = 0; u < NV; ++u) {
+      const uint4 q = lds128(cb + (v + u * kFT) * 16);
+      w[4 * u] = q.x; w[4 * u + 1] = q.y; w[4 * u + 2] = q.z; w[4 * u + 3] = q.w;
+    }
+    uint32_t m2 = hmax2(w[0], w[1]);
 #pragma unroll
-    for (int e = 1; e < 8 * NV; ++e) lm = fmaxf(lm, z[e]);
+    for (int k = 2; k < 4 * NV; ++k) m2 = hmax2(m2, w[k]);
+    const float lm = fmaxf(bf16_lo(m2), bf16_hi(m2));
     if (lm > mz) {
       const float f = ex2f_approx((mz - lm) * c);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) s[j] *= f;
+      s[0] = __fmul2_rn(s[0], make_float2(f, f));
+      s[1] = __fmul2_rn(s[1], make_float2(f, f));
       mz = lm;
       nb = -mz * c;
     }
 #pragma unroll
-    for (int e = 0; e < 8 * NV; ++e) s[e & 3] += ex2f_approx(fmaf(z[e], c, nb));
+    for (int k = 0; k < 4 * NV; ++k) {
+      const float2 t = __ffma2_rn(bf16x2_f32(w[k]), make_float2(c, c), make_float2(nb, nb));
+      s[k & 1] = __fadd2_rn(s[k & 1], make_float2(ex2f_approx(t.x), ex2f_approx(t.y)));
+    }
   }
   __device__ __forceinline__ void chunk(const uint8_t* cb, uint32_t bytes, float c, int tid) {
     const uint32_t nv = bytes / 16;
@@ -131,21 +148,23 @@ struct RowAcc {
     for (; v + kFT < nv; v += 2 * kFT) step<2>(cb, v, c);
     if (v < nv) step<1>(cb, v, c);
   }
-  __device__ __forceinline__ float sum() const { return (s[0] + s[1]) + (s[2] + s[3]); }
+  __device__ __forceinline__ float sum() const { return (s[0].x + s[0].y) + (s[1].x + s[1].y); }
 };
 
-// Pass 2 over one chunk: grad = -cf * 2^(z c + nl) (the one-hot term is patched by the owner thread).
+// Pass 2 over one chunk: grad = -cf * 2^(z c + nl) (the one-hot term is patched by the owner thread),
+// exponent arguments and scaling in f32x2.
 template <int NV>
 __device__ __forceinline__ void grad_step(const uint8_t* cb, uint32_t v, float c, float ncf, float nl, uint16_t* gout) {
 #pragma unroll
   for (int u = 0; u < NV; ++u) {
-    float z[8];
-    unpack8(lds128(cb + (v + u * kFT) * 16), z);
+    const uint4 q = lds128(cb + (v + u * kFT) * 16);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      __nv_bfloat162 p2 = __floats2bfloat162_rn(ncf * ex2f_approx(fmaf(z[2 * e], c, nl)),
-                                                ncf * ex2f_approx(fmaf(z[2 * e + 1], c, nl)));
+      const float2 t = __ffma2_rn(bf16x2_f32(w[e]), make_float2(c, c), make_float2(nl, nl));
+      const float2 g = __fmul2_rn(make_float2(ex2f_approx(t.x), ex2f_approx(t.y)), make_float2(ncf, ncf));
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(g.x, g.y);
       o[e] = *reinterpret_cast<uint32_t*>(&p2);
     }
     stg128_stream(gout + (uint64_t)(v + u * kFT) * 8, make_uint4(o[0], o[1], o[2], o[3]));
