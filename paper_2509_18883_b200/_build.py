@@ -40,10 +40,22 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every kernel TU and link `_rlk.so`; returns its path. Incremental unless force."""
+LIB_CHECKED = PKG / "_rlk_checked.so"
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = True) -> Path:
+    """Compile every kernel TU and link `_rlk.so` (and the RLK_CHECKED assert build `_rlk_checked.so`
+    that tests/test_gpu_checked.py runs the GPU suite against); returns the release library's path.
+    Incremental unless force."""
+    lib = _build_one(LIB, BUILD, [], force, verbose)
+    if checked:
+        _build_one(LIB_CHECKED, BUILD / "checked", ["-DRLK_CHECKED"], force, verbose)
+    return lib
+
+
+def _build_one(LIB: Path, BUILD: Path, extra: list, force: bool, verbose: bool) -> Path:
     nvcc = _nvcc()
-    BUILD.mkdir(exist_ok=True)
+    BUILD.mkdir(parents=True, exist_ok=True)
     headers = sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [INCLUDE / "rlk.h"]
     jobs = []
     objs = []
@@ -51,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = BUILD / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src] + headers):
-            jobs.append([nvcc, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)])
+            jobs.append([nvcc, *NVCC_FLAGS, *extra, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)])
     for src in CPP_SOURCES:
         if not (CSRC / src).exists():
             continue

@@ -5,6 +5,7 @@
 //  * mbarrier + cp.async.bulk (TMA bulk copy, SASS UBLKCP) ring-pipeline primitives
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -15,6 +16,26 @@
 #endif
 
 namespace rlk {
+
+// ---------------------------------------------------------------- checked builds
+// RLK_CHECKED (tools/build_variant.py checked -DRLK_CHECKED): device-side bounds / alignment asserts on
+// every TMA copy and shared-memory index of the streaming kernels, and a poll limit on every mbarrier
+// wait (a lost arrival traps instead of hanging the GPU).  This pool disables compute-sanitizer; the
+// GPU test suite runs against this build instead (tests/test_gpu_checked.py).  Release builds: no-ops.
+#ifdef RLK_CHECKED
+#define RLK_DCHECK(cond)                                                                             \
+  do {                                                                                               \
+    if (!(cond)) {                                                                                   \
+      printf("RLK_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,        \
+             (int)blockIdx.x, (int)threadIdx.x);                                                     \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#else
+#define RLK_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- SplitMix64 (core.py:26-33, 42-49)
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
@@ -104,6 +125,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+#ifdef RLK_CHECKED
+  for (uint64_t polls = 0;; ++polls) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    RLK_DCHECK(polls < (1ull << 26));  // each try_wait suspends up to a hardware time limit: ~seconds
+  }
+#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -126,8 +159,22 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 // 1-D TMA bulk copy global -> shared, completion signalled on `bar` (complete_tx::bytes).
 // dst / src / bytes must be 16-byte aligned / multiples of 16.
+__device__ __forceinline__ uint32_t total_smem_bytes() {
+  uint32_t r;
+  asm("mov.u32 %0, %%total_smem_size;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t dynamic_smem_bytes() {
+  uint32_t r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
+  RLK_DCHECK(bytes > 0 && bytes % 16 == 0 && ((uintptr_t)src & 15u) == 0 && (smem_u32(dst) & 15u) == 0);
+  // the CTA's offset in its shared window (a cluster CTA's window carries its rank above bit 24), within
+  // the CTA's allocation (+ the 1 KiB system reservation)
+  RLK_DCHECK((smem_u32(dst) & 0x00ffffffu) + bytes <= total_smem_bytes() + 1024u);
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
       "%4;" ::"r"(smem_u32(dst)),

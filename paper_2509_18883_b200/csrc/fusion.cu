@@ -138,6 +138,10 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
       mbar_wait(&r.empty[s], ph ^ 1u);
       const uint32_t tx = main_bytes * ns + bm_bytes * N;
       uint8_t* dst = r.buf + s * r.stage_bytes;
+      RLK_DCHECK(s < r.nstages && off + n <= g.len && g.start + g.len <= g.seg->numel);
+      RLK_DCHECK(main_bytes <= SB && ns * SB <= r.stage_bytes);
+      RLK_DCHECK(!bitmap || ((N + 1) * SB + N * BMB <= r.stage_bytes && bm_bytes <= BMB));
+      RLK_DCHECK(!bm_bytes || (jtensor0 + off) / 8 + bm_bytes <= words_per_row * 4);
       if (tx) {
         mbar_arrive_expect_tx(&r.full[s], tx);
         if (main_bytes) {
@@ -968,6 +972,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
       uint32_t slowbits = 0;
       auto vec = [&](const uint32_t v, const uint32_t jit) {
         const uint32_t le = v * kFastElems;
+        RLK_DCHECK(le + kFastElems <= main_elems && jit + kFastElems <= 32);
         const FastVec bw4 = FastVec::load(sb + v * (2 * kFastElems));
         FastVec xw4[N];
         uint32_t kb[N];
@@ -1141,6 +1146,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         const uint32_t bpos = __ffs(slowbits) - 1;
         slowbits &= slowbits - 1;
         const uint32_t le = (tid + (bpos / kFastElems) * kFastCThreads) * kFastElems + (bpos % kFastElems);
+        RLK_DCHECK(le < main_elems && off + le < g.len);
         const float be = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(sb)[le] << 16);
         FArr<N> xe;
         uint32_t keep = 0;

@@ -157,6 +157,7 @@ template <int NV>
 __device__ __forceinline__ void grad_step(const uint8_t* cb, uint32_t v, float c, float ncf, float nl, uint16_t* gout) {
 #pragma unroll
   for (int u = 0; u < NV; ++u) {
+    RLK_DCHECK((v + u * kFT) * 16 < kChunkBytes);
     const uint4 q = lds128(cb + (v + u * kFT) * 16);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t o[4];
@@ -250,6 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         const char* src = a.logits + (lrow(row) * a.row_stride + v0) * 2;
         for (uint32_t k = 0; k < nch; ++k) {
           const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
+          RLK_DCHECK(q.s < nslots && bytes > 0 && (uint64_t)k * kChunkBytes + bytes <= half_bytes);
           mbar_wait(&empty[q.s], q.ph ^ 1u);
           mbar_arrive_expect_tx(&full[q.s], bytes);
           bulk_g2s(buf + q.s * kChunkBytes, src + (uint64_t)k * kChunkBytes, bytes, &full[q.s], pol);
@@ -304,6 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       }
       warp_combine(M, S, c);
       if (lane == 0) {
+        RLK_DCHECK(p < 2 && peer < 2);
         st_async_peer(mapa(smem_u32(&slot[p]), peer), M, S, mapa(smem_u32(&xbar[p]), peer));
         mbar_wait(&xbar[p], ph[p]);
         const float2 o = slot[p];

@@ -12,4 +12,4 @@ B.NVCC_FLAGS = B.NVCC_FLAGS + flags
 B.BUILD = ROOT / "build" / ("var_" + name)
 B.LIB = ROOT / "tools" / "var" / f"_rlk_{name}.so"
 B.LIB.parent.mkdir(parents=True, exist_ok=True)
-print(B.build(force=True))
+print(B.build(force=True, checked=False))
