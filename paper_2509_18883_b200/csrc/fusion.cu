@@ -107,7 +107,7 @@ __device__ __forceinline__ ItemGeom item_geom(const rlk_fusion_plan& plan, SegCu
 // binary search per item (K1: measured faster there, same-box A/B)
 template <int ESZ, int N, uint32_t SB = StreamBytes<N>::v, bool kCursor = true>
 __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_base, const uint32_t* bitmap,
-                        uint64_t words_per_row) {
+                        uint64_t words_per_row, uint32_t sub_shift = 0) {
   constexpr uint32_t ELEMS = SB / ESZ;
   constexpr uint32_t BMB = ELEMS / 8;  // bitmap bytes per expert per full stage
   const int ns = with_base ? N + 1 : N;
@@ -118,8 +118,13 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
   const uint64_t pol_bm = policy_evict_last();
   RingPos q;
   SegCursor cur;
-  for (uint32_t item = blockIdx.x; item < plan.n_items; item += gridDim.x) {
+  const uint32_t unit = kItem >> sub_shift;
+  for (uint32_t u = blockIdx.x; u < (plan.n_items << sub_shift); u += gridDim.x) {
+    const uint32_t item = u >> sub_shift;
     const ItemGeom g = kCursor ? item_geom(plan, cur, item) : item_geom_bs(plan, item);
+    const uint32_t lo = (u & ((1u << sub_shift) - 1u)) * unit;  // the unit's element range [lo, hi)
+    if (lo >= g.len) continue;
+    const uint32_t hi = min(g.len, lo + unit);
     const char* src[N + 1];
     if (!with_base) {
 #pragma unroll
@@ -130,15 +135,15 @@ __device__ void produce(const rlk_fusion_plan& plan, const Ring& r, bool with_ba
       for (int i = 0; i < N; ++i) src[i + 1] = (const char*)g.seg->expert[i];
     }
     const uint64_t jtensor0 = g.j0 + g.start;
-    for (uint32_t off = 0; off < g.len; off += ELEMS) {
-      const uint32_t n = min(ELEMS, g.len - off);
+    for (uint32_t off = lo; off < hi; off += ELEMS) {
+      const uint32_t n = min(ELEMS, hi - off);
       const uint32_t main_bytes = (n * ESZ) & ~15u;
       const uint32_t bm_bytes = bitmap ? (((n + 7) / 8 + 15) & ~15u) : 0u;
       const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.empty[s], ph ^ 1u);
       const uint32_t tx = main_bytes * ns + bm_bytes * N;
       uint8_t* dst = r.buf + s * r.stage_bytes;
-      RLK_DCHECK(s < r.nstages && off + n <= g.len && g.start + g.len <= g.seg->numel);
+      RLK_DCHECK(s < r.nstages && off + n <= hi && hi <= g.len && g.start + g.len <= g.seg->numel);
       RLK_DCHECK(main_bytes <= SB && ns * SB <= r.stage_bytes);
       RLK_DCHECK(!bitmap || ((N + 1) * SB + N * BMB <= r.stage_bytes && bm_bytes <= BMB));
       RLK_DCHECK(!bm_bytes || (jtensor0 + off) / 8 + bm_bytes <= words_per_row * 4);
@@ -561,6 +566,7 @@ struct MergeArgs {
   int dropout_mode, erase_mode, delta_mode, with_base, fast;
   uint32_t stage_bytes, nstages;
   const uint32_t* bitmap;
+  uint32_t sub_shift;  // K3 work unit = 1 / 2^sub_shift of an item (small layouts: more CTAs busy)
 };
 
 struct ElemConsts {
@@ -699,14 +705,20 @@ __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid
   const bool wb = a.with_base != 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kCWarps) {
-    if (lane == 0) produce<ESZ, N>(a.plan, r, wb, a.dropout_mode == 2 ? a.bitmap : nullptr, a.words_per_row);
+    if (lane == 0)
+      produce<ESZ, N>(a.plan, r, wb, a.dropout_mode == 2 ? a.bitmap : nullptr, a.words_per_row, a.sub_shift);
     return;
   }
   const int tid = threadIdx.x;
   RingPos q;
   SegCursor cur;
-  for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
+  const uint32_t unit = kItem >> a.sub_shift;
+  for (uint32_t u = blockIdx.x; u < (a.plan.n_items << a.sub_shift); u += gridDim.x) {
+    const uint32_t item = u >> a.sub_shift;
     const ItemGeom g = item_geom(a.plan, cur, item);
+    const uint32_t lo = (u & ((1u << a.sub_shift) - 1u)) * unit;
+    if (lo >= g.len) continue;
+    const uint32_t hi = min(g.len, lo + unit);
     const double* scale = a.scale + (uint64_t)g.tensor * N;
     ElemConsts c;
 #pragma unroll
@@ -715,8 +727,8 @@ __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid
 #pragma unroll
     for (int i = 0; i < N; ++i) cnt_er[i] = 0;
     const uint64_t jtensor0 = g.j0 + g.start;
-    for (uint32_t off = 0; off < g.len; off += ELEMS) {
-      const uint32_t n = min(ELEMS, g.len - off);
+    for (uint32_t off = lo; off < hi; off += ELEMS) {
+      const uint32_t n = min(ELEMS, hi - off);
       const uint32_t main_elems = ((n * ESZ) & ~15u) / ESZ;
       const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.full[s], ph);
@@ -900,7 +912,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
   const Ring r = ring_setup(smem, a.stage_bytes, a.nstages, kFastCWarps);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kFastCWarps) {
-    if (lane == 0) produce<2, N, kFastSB>(a.plan, r, true, DROP == 2 ? a.bitmap : nullptr, a.words_per_row);
+    if (lane == 0) produce<2, N, kFastSB>(a.plan, r, true, DROP == 2 ? a.bitmap : nullptr, a.words_per_row, a.sub_shift);
     return;
   }
   const int tid = threadIdx.x;
@@ -935,8 +947,13 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
   float sr32[N];
   bool fast_ok = false;
   uint32_t c_tensor = 0xffffffffu;  // tensor whose scales are loaded
-  for (uint32_t item = blockIdx.x; item < a.plan.n_items; item += gridDim.x) {
+  const uint32_t unit = kItem >> a.sub_shift;
+  for (uint32_t u = blockIdx.x; u < (a.plan.n_items << a.sub_shift); u += gridDim.x) {
+    const uint32_t item = u >> a.sub_shift;
     const ItemGeom g = item_geom(a.plan, cur, item);
+    const uint32_t lo = (u & ((1u << a.sub_shift) - 1u)) * unit;
+    if (lo >= g.len) continue;
+    const uint32_t hi = min(g.len, lo + unit);
     const double* scale = a.scale + (uint64_t)g.tensor * N;
     uint16_t* const outp = (uint16_t*)g.out;
     if (g.tensor != c_tensor) {  // per-tensor constants: reloaded only when the tensor changes
@@ -956,8 +973,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 #pragma unroll
     for (int i = 0; i < N; ++i) cnt_er[i] = 0;
     const uint64_t jtensor0 = g.j0 + g.start;
-    for (uint32_t off = 0; off < g.len; off += ELEMS) {
-      const uint32_t n = min(ELEMS, g.len - off);
+    for (uint32_t off = lo; off < hi; off += ELEMS) {
+      const uint32_t n = min(ELEMS, hi - off);
       const uint32_t main_elems = ((n * 2) & ~15u) / 2;
       const uint32_t s = q.s, ph = q.ph;
       mbar_wait(&r.full[s], ph);
@@ -1198,6 +1215,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 }
 
 // ------------------------------------------------------------------ host-side launch helpers
+// K3 work-unit split for layouts with fewer items than ~2 waves of CTAs (config 1: 154 items on 296
+// CTA slots): 2^s units per item, at most one ring stage per unit apart (`stages_per_item`), so every
+// CTA slot gets work.  Large layouts keep whole items (s = 0).
+static uint32_t sub_shift_for(uint32_t n_items, uint32_t cap, uint32_t stages_per_item) {
+  uint32_t s = 0;
+  while (s < 3 && (n_items << s) < 2 * cap && (1u << (s + 1)) <= stages_per_item) ++s;
+  return s;
+}
+
 template <int N>
 static void stage_geometry(int esz, bool bitmap, uint32_t& stage_bytes, uint32_t& nstages) {
   const uint32_t sb = StreamBytes<N>::v;
@@ -1246,7 +1272,9 @@ static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
   auto kern = k_merge_fast<N, DROP, ERASE, UNI>;
   int st = ensure_smem(kern, smem);
   if (st) return st;
-  uint32_t grid = std::min<uint32_t>(a.plan.n_items, kFastCtas * (uint32_t)sm_count());
+  const uint32_t cap = kFastCtas * (uint32_t)sm_count();
+  a.sub_shift = sub_shift_for(a.plan.n_items, cap, kItem / kFastSB * 2);
+  uint32_t grid = std::min<uint32_t>(a.plan.n_items << a.sub_shift, cap);
   kern<<<grid, kFastThreads, smem, s>>>(a);
   return launch_status("rlk_fusion_merge");
 }
@@ -1283,7 +1311,9 @@ static int launch_merge(MergeArgs& a, cudaStream_t s) {
   auto kern = k_merge<DTI, DTO, N>;
   int st = ensure_smem(kern, smem);
   if (st) return st;
-  uint32_t grid = std::min<uint32_t>(a.plan.n_items, ctas * (uint32_t)sm_count());
+  const uint32_t cap = ctas * (uint32_t)sm_count();
+  a.sub_shift = sub_shift_for(a.plan.n_items, cap, kItem / StreamBytes<N>::v * Elem<DTI>::size);
+  uint32_t grid = std::min<uint32_t>(a.plan.n_items << a.sub_shift, cap);
   kern<<<grid, kThreads, smem, s>>>(a);
   return launch_status("rlk_fusion_merge");
 }
@@ -1422,7 +1452,7 @@ int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, i
               "rlk_fusion_merge: bitmap mode needs a bitmap with 16-byte rows");
   RLK_REQUIRE(dropout_mode == 0 || (keep_prob > 0.0 && keep_prob <= 1.0), "rlk_fusion_merge: bad keep_prob");
   if (plan->n_items == 0) return RLK_OK;
-  MergeArgs a;
+  MergeArgs a{};
   memset(&a, 0, sizeof(a));
   a.plan = *plan;
   a.scale = scale;
