@@ -687,6 +687,89 @@ __device__ __forceinline__ uint32_t fast_opp_bits(float b, const float* x, uint3
   return m;
 }
 
+// Phase-2 resolver: one flagged element re-evaluated in scalar f32 -- the fast path's certification
+// is per pair (a failed vote margin flags both elements), so most flagged elements are certifiable on
+// their own.  ERASE 0 / 1 only (the squared vote keeps the f64 path).  Returns
+//   1: certified like the fast path (same vote-sign and output-bracket arguments); the fast loop's
+//      erased count for this element stands;
+//   2: an exact sum-vote tie, certified: with every scale an exact power of two and no dropout or a
+//      power-of-two keep probability (`tie_ok`), k_i = d_i * sr is exact in f32 when the non-zero
+//      members of {b, kept x_i} span at most 13 binades (d_i then needs <= 22 bits), and so are the
+//      vote's partial sums (< 2^24 quanta); the reference's f64 k_i and vote are exact too.  A vote
+//      computed as exactly 0 is then a true tie (fusion.py:136-141: sign(0) = 0 erases nothing), and
+//      `fast_opp` is what the fast loop counted as erased (t = k * sign(+0) < 0), to be undone;
+//   0: not certifiable here -- the caller runs the reference-order f64 path.
+// sr32 / w32 / wh32 / wmax are the kernel's scaled-domain constants (k' = k 2^24, w' = w 2^-24).
+template <int N, int ERASE, bool UNI>
+__device__ __forceinline__ int scalar_resolve(uint32_t bbits, const uint32_t* xbits, uint32_t keep, const float* sr32,
+                                              const float* w32, const float* wh32, float wmax, bool tie_ok,
+                                              uint16_t* out, uint32_t* fast_opp) {
+  const float be = __uint_as_float(bbits << 16);
+  float k[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    k[i] = __fmul_rn(fmaf(be, -1.f, __uint_as_float(xbits[i] << 16)), ((keep >> i) & 1u) ? sr32[i] : 0.f);
+  float aa = N == 1 ? fabsf(k[0]) : __fadd_rn(fabsf(k[0]), fabsf(k[1]));
+#pragma unroll
+  for (int i = 2; i < N; ++i) aa = __fadd_rn(aa, fabsf(k[i]));
+  const float S = fmaf(wmax, aa, __fadd_rn(fabsf(be), 0x1p-110f));
+  float y;
+  int kind = 1;
+  if constexpr (ERASE == 1 && N >= 2) {
+    float vv = k[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) vv = __fadd_rn(vv, k[i]);
+    if (fmaf(-0x1p-20f, aa, fabsf(vv)) < 0.f || !(aa < INFINITY)) {  // vote sign not certain here
+      if (!(tie_ok && vv == 0.f)) return 0;
+      uint32_t emax = 0, emin = 0xffu;
+      auto span = [&](uint32_t h) {
+        if (h & 0x7fffu) {
+          const uint32_t e = max((h >> 7) & 0xffu, 1u);  // subnormals: the ulp of binade 1
+          emax = max(emax, e);
+          emin = min(emin, e);
+        }
+      };
+      span(bbits);
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        if ((keep >> i) & 1u) span(xbits[i]);
+      if (emax < emin || emax - emin > 13u) return 0;
+      // a true tie: nothing erased, y = b + sum_i w_i k_i
+      y = be;
+      uint32_t fo = 0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        y = fmaf(w32[i], k[i], y);
+        fo |= (uint32_t)(k[i] < 0.f) << i;
+      }
+      *fast_opp = fo;
+      kind = 2;
+    } else {
+      const float sg = copysignf(1.f, vv);
+      if constexpr (UNI) {
+        y = fmaf(wh32[0], fmaf(sg, aa, vv), be);
+      } else {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const float t = fmaf(k[i], sg, 0.f);
+          acc = fmaf(wh32[i], __fadd_rn(t, fabsf(t)), acc);
+        }
+        y = fmaf(sg, acc, be);
+      }
+    }
+  } else {
+    y = be;
+#pragma unroll
+    for (int i = 0; i < N; ++i) y = fmaf(w32[i], k[i], y);
+  }
+  if (!(fabsf(y) < INFINITY)) return 0;
+  const uint16_t lo = f32_to_bf16_rne(fmaf(-0x1p-20f, S, y)), hi = f32_to_bf16_rne(fmaf(0x1p-20f, S, y));
+  if (lo != hi) return 0;
+  *out = lo;
+  return kind;
+}
+
 __device__ __forceinline__ uint32_t word_of(const uint4& q, int p) {
   return p == 0 ? q.x : (p == 1 ? q.y : (p == 2 ? q.z : q.w));
 }
@@ -945,8 +1028,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
   SegCursor cur;
   ElemConsts c;
   float sr32[N];
-  bool fast_ok = false;
+  bool fast_ok = false, tie_ok = false;
   uint32_t c_tensor = 0xffffffffu;  // tensor whose scales are loaded
+  // exact ties need power-of-two keep scaling (checked on the f64 value the reference divides by)
+  const bool keep_pow2 = !DROP || (__double_as_longlong(a.keep_prob) & 0xfffffffffffffull) == 0;
   const uint32_t unit = kItem >> a.sub_shift;
   for (uint32_t u = blockIdx.x; u < (a.plan.n_items << a.sub_shift); u += gridDim.x) {
     const uint32_t item = u >> a.sub_shift;
@@ -959,6 +1044,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
     if (g.tensor != c_tensor) {  // per-tensor constants: reloaded only when the tensor changes
       c_tensor = g.tensor;
       fast_ok = w_ok;
+      tie_ok = ERASE == 1 && keep_pow2;
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         c.scale[i] = __ldg(scale + i);
@@ -966,6 +1052,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         // k = d * sr cannot underflow for bf16 deltas (|d| >= 2^-133) when sr >= 2^-16; sr < 2^100
         // keeps sr * 2^24 finite
         fast_ok = fast_ok && sr32[i] >= 0x1p-16f && sr32[i] < 0x1p100f;
+        // tie resolution: every scale an exact power of two (f64 mantissa zero), hence all sr exact
+        tie_ok = tie_ok && (__double_as_longlong(c.scale[i]) & 0xfffffffffffffull) == 0 && c.scale[i] > 0.0;
         sr32[i] *= kKS;
       }
     }
@@ -1171,6 +1259,22 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         for (int i = 0; i < N; ++i) {
           xe.v[i] = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le] << 16);
           keep |= DROP ? (((uint32_t)bm[i * BMB + (le >> 3)] >> (le & 7)) & 1u) << i : (1u << i);
+        }
+        if constexpr (ERASE != 2) {
+          uint32_t xb[N], fo = 0;
+          uint16_t wout;
+#pragma unroll
+          for (int i = 0; i < N; ++i) xb[i] = reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le];
+          const int kind = scalar_resolve<N, ERASE, UNI>(reinterpret_cast<const uint16_t*>(sb)[le], xb, keep, sr32,
+                                                         w32, wh32, wmax, tie_ok, &wout, &fo);
+          if (kind) {
+            if (kind == 2) {
+#pragma unroll
+              for (int i = 0; i < N; ++i) cnt_er[i] -= (fo >> i) & 1u;
+            }
+            outp[out_base + le] = wout;
+            continue;
+          }
         }
         uint32_t nzm, erm;
         const double Y = merge_elem_slow<N>(be, xe, keep, &a, scale, &nzm, &erm);

@@ -211,7 +211,8 @@ def test_fast_path_equals_exact_path_random(cuda, monkeypatch):
     d1 = experts[1].float()[idx] - base.float()[idx]
     experts[2][idx] = (base.float()[idx] - d0 - d1).to(torch.bfloat16)
     for cfg in (F.FusionConfig(), F.FusionConfig(dropout_p=0.5, seed=1), F.FusionConfig(erase_weighting="squared"),
-                F.FusionConfig(target_norm=None)):
+                F.FusionConfig(target_norm=None), F.FusionConfig(target_norm=None, dropout_p=0.5, seed=2),
+                F.FusionConfig(target_norm=None, dropout_p=0.75, seed=3, merge_weights=(0.5, 0.25, 0.25))):
         outs = []
         for exact in (False, True):
             o, rep = F.fuse_state_dict({"w": base}, [{"w": e} for e in experts], cfg, exact_merge=exact)
