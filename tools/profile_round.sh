@@ -1,10 +1,12 @@
 #!/bin/bash
-# Round evidence (run on the GPU box): full bench line, ncu launch list of the bench command (our
-# kernels only), ncu --set full of the fusion and GRPO kernels.
+# Round evidence (run on the GPU box): full bench line (config 3 headline + configs 1/2 sub-results +
+# GRPO config 5 + CPU baselines), ncu launch list of the bench command (our kernels only), ncu --set
+# full of the fusion and GRPO kernels, the config-4 streaming slice, the reference arm.
 set -x
-OUT=gpurun_out/${1:-r01}
+OUT=gpurun_out/${1:-r02}
 mkdir -p $OUT
 python bench.py --steps 10 --warmup 3 --json-out $OUT/bench.json > $OUT/bench.log 2>&1
+python bench.py --impl reference > $OUT/bench_reference.log 2>&1
 Q="python bench.py --steps 3 --warmup 3 --quick --no-e2e --no-cpu"
 K='regex:k_sumsq|k_merge|k_mask_bitmap|k_finalize|k_grpo|k_segment_sum'
 $Q > $OUT/quick_plain.log 2>&1 && \
@@ -13,9 +15,5 @@ python tools/prof_fusion.py --layout llama8b --runs 2 > $OUT/prof_plain.log 2>&1
 ncu --set full --clock-control none --import-source on -k "regex:k_merge_fast|k_sumsq_bf16|k_mask_bitmap" -s 3 -c 3 -o $OUT/fusion_full python tools/prof_fusion.py --layout llama8b --runs 2 > $OUT/ncu_fusion.log 2>&1
 python tools/prof_grpo_fused.py > $OUT/prof_grpo_plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k "regex:k_grpo" -s 4 -c 4 -o $OUT/grpo_full python tools/prof_grpo_fused.py > $OUT/ncu_grpo.log 2>&1
-# other BASELINE configs: 2 (GPT-1.3B-shaped) and 1 (10M MLP) bench lines, config-4 streaming slices
-python bench.py --steps 10 --warmup 3 --layout gpt1p3b --no-grpo --no-cpu --json-out $OUT/bench_config2.json > $OUT/bench_config2.log 2>&1
-python bench.py --steps 10 --warmup 3 --layout mlp10m --dtype f32 --no-grpo --no-cpu --json-out $OUT/bench_config1.json > $OUT/bench_config1.log 2>&1
-python tools/bench_streaming.py --layers 1 --source replay --json-out $OUT/config4_replay.json > $OUT/config4_replay.log 2>&1
-python tools/bench_streaming.py --layers 1 --source pinned --json-out $OUT/config4_pinned.json > $OUT/config4_pinned.log 2>&1
+python bench.py --stream --stream-layers 1 --steps 3 --warmup 3 --json-out $OUT/config4_stream.json > $OUT/config4_stream.log 2>&1
 ls -la $OUT

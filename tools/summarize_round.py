@@ -20,9 +20,14 @@ dst = ROOT / "profiles"
 
 # 1. bench lines (config 3 headline; configs 1, 2 and the config-4 streaming slices when present)
 shutil.copy(src / "bench.json", dst / f"{tag}_bench.json")
-for extra in ("bench_config2.json", "bench_config1.json", "config4_replay.json", "config4_pinned.json"):
+for extra in ("bench_config2.json", "bench_config1.json", "config4_replay.json", "config4_pinned.json",
+              "config4_stream.json"):
     if (src / extra).exists():
         shutil.copy(src / extra, dst / f"{tag}_{extra}")
+if (src / "bench_reference.log").exists():
+    ref = [l for l in (src / "bench_reference.log").read_text().splitlines() if l.startswith("{")]
+    if ref:
+        (dst / f"{tag}_bench_reference.json").write_text(json.dumps(json.loads(ref[-1]), indent=1))
 
 # 2. launch list -> per-kernel averages and the fusion-step shares
 rows = list(csv.reader(open(src / "launches.csv")))
