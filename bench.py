@@ -434,7 +434,45 @@ def grpo_bench(args, rank, world, local, group):
                            "ragged_lengths": variant(ragged=True)}
     del logits
     torch.cuda.empty_cache()
+    if not args.quick:
+        out["variants"]["f32_logits"] = grpo_f32_variant(args, batch, rows, V, n_chunks, G * T, stream, dev, group)
     return out
+
+
+def grpo_f32_variant(args, batch, rows, V, n_chunks, tokens, stream, dev, group) -> dict:
+    """Config 5 with f32 logits (as trainers that upcast the LM head produce): the one-read fused loss +
+    gradient on 4-CTA clusters (8 B/logit: f32 read + f32 grad write) against K4 + K5 (12 B/logit)."""
+    import torch
+    from paper_2509_18883_b200 import _lib as L
+    from paper_2509_18883_b200 import objective as O
+    lg = torch.empty((rows, V), dtype=torch.float32, device=dev)
+    L.call("rlk_synth_normal", L.ptr(lg), L.RLK_F32, lg.numel(), 0, 4321, 2.0, None, L.stream_handle(stream))
+    res = {}
+    for name, fn in (("fused", lambda: O.grpo_forward_backward(lg, batch, stream=stream)),
+                     ("k4_k5", lambda: O.grpo_backward(lg, batch, O.grpo_forward(lg, batch, stream=stream),
+                                                       stream=stream))):
+        for _ in range(args.warmup):
+            fn()
+        barrier(group)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            for _ in range(n_chunks):
+                fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms, = max_over_ranks([e0.elapsed_time(e1) / args.steps], group)
+        res[f"{name}_ms"] = ms
+        res[f"{name}_tokens_per_s"] = tokens / (ms / 1e3)
+    peak, _ = measured_peak_gbs()
+    per_launch = res["fused_ms"] / n_chunks
+    res["fused_roofline"] = {"bytes_per_token": V * 8, "achieved": rows * V * 8 / (per_launch / 1e3) / 1e9,
+                             "peak": peak, "unit": "GB/s",
+                             "frac": rows * V * 8 / (per_launch / 1e3) / 1e9 / peak}
+    del lg
+    torch.cuda.empty_cache()
+    return res
 
 
 # ----------------------------------------------------------------------------------- CPU baseline

@@ -20,6 +20,7 @@
  *   rlk_segment_sum_f64     per-group token-term sums                objective.py:238-250
  *   rlk_grpo_bwd            objective_gradient                       objective.py:253-283
  *   rlk_grpo_fused_bf16     objective_value + objective_gradient     objective.py:230-283 (one pass)
+ *   rlk_grpo_fused          the same for bf16 or f32 logits          objective.py:230-283 (one pass)
  *   rlk_logsoftmax_rows     log_token_dist (full row)                toy_env.py:157-175
  *   rlk_nonfinite_count     ParamTable finite check                  toy_env.py:71-72
  *   rlk_scaled_add          ascent_step (params + lr * grad)         objective.py:286-293
@@ -156,6 +157,17 @@ int rlk_grpo_fused_bf16(const void* logits, uint64_t n_rows, uint64_t vocab, uin
                         const rlk_clip* clip, double grad_scale, double* logp_out, double* lse_out,
                         double* term, double* coef, int32_t* flags, void* grad, uint64_t grad_row_stride,
                         void* stream);
+
+/* The same for bf16 (2-CTA clusters, gradient bf16) or f32 logits (4-CTA clusters -- each CTA owns a
+ * quarter row of 128 KiB -- gradient f32): 8 B of HBM traffic per f32 logit instead of 12 for
+ * rlk_grpo_fwd + rlk_grpo_bwd.  vocab % (8 * cluster) == 0 and vocab <= 204800 (bf16) / 204800 (f32). */
+int rlk_grpo_fused(const void* logits, int dtype, uint64_t n_rows, uint64_t vocab, uint64_t row_stride,
+                   const int64_t* row_index, const int32_t* tokens, const double* logp_train,
+                   const double* logp_infer, const int32_t* sample_of_row, const double* adv,
+                   const uint8_t* use, const double* temperature, const double* norm,
+                   const rlk_clip* clip, double grad_scale, double* logp_out, double* lse_out,
+                   double* term, double* coef, int32_t* flags, void* grad, uint64_t grad_row_stride,
+                   void* stream);
 
 /* out[g] = sum of x[seg_ptr[g] .. seg_ptr[g+1]) in a fixed order (one block per segment). */
 int rlk_segment_sum_f64(const double* x, const int64_t* seg_ptr, uint64_t n_segs, double* out, void* stream);

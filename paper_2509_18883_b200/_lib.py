@@ -61,6 +61,8 @@ SIGNATURES = {
     "rlk_segment_sum_f64": (_I, [_P, _P, _U64, _P, _P]),
     "rlk_grpo_fused_bf16": (_I, [_P, _U64, _U64, _U64, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.POINTER(ClipC), _D,
                                  _P, _P, _P, _P, _P, _P, _U64, _P]),
+    "rlk_grpo_fused": (_I, [_P, _I, _U64, _U64, _U64, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.POINTER(ClipC), _D,
+                            _P, _P, _P, _P, _P, _P, _U64, _P]),
     "rlk_grpo_bwd": (_I, [_P, _I, _U64, _U64, _U64, _P, _P, _P, _P, _P, _P, _P, _P, _I, _U64, _P]),
     "rlk_logsoftmax_rows": (_I, [_P, _I, _U64, _U64, _U64, _P, _P, _P, _I, _P]),
     "rlk_nonfinite_count": (_I, [_P, _I, _U64, _P, _P]),

@@ -1,4 +1,5 @@
-// Fused single-pass GRPO forward + backward for bf16 logits (K4+K5 in one read of the logits).
+// Fused single-pass GRPO forward + backward (K4+K5 in one read of the logits): bf16 logits on 2-CTA
+// clusters, f32 logits on 4-CTA clusters (each CTA owns V / cluster elements of the row: 128 KiB).
 //
 // objective_value and objective_gradient (pkg/src/rolloutlab/objective.py:230-283) both need the
 // row's log-sum-exp; the backward additionally needs coef = norm * w * slope * r / T, known only after
@@ -13,6 +14,8 @@
 #include "common.cuh"
 #include "capi_internal.h"
 #include "pipeline.cuh"
+
+#include <type_traits>
 
 namespace rlk {
 
@@ -73,7 +76,7 @@ struct FusedArgs {
   double grad_scale;
   double *logp, *lse, *term, *coef;
   int32_t* flags;
-  uint16_t* grad;
+  void* grad;
   uint64_t grad_row_stride;
   uint32_t nslots;
 };
@@ -129,24 +132,51 @@ struct RowAcc {
 #pragma unroll
     for (int k = 2; k < 4 * NV; ++k) m2 = hmax2(m2, w[k]);
     const float lm = fmaxf(bf16_lo(m2), bf16_hi(m2));
-    if (lm > mz) {
-      const float f = ex2f_approx((mz - lm) * c);
-      s[0] = __fmul2_rn(s[0], make_float2(f, f));
-      s[1] = __fmul2_rn(s[1], make_float2(f, f));
-      mz = lm;
-      nb = -mz * c;
-    }
+    if (lm > mz) rescale(lm, c);
 #pragma unroll
     for (int k = 0; k < 4 * NV; ++k) {
       const float2 t = __ffma2_rn(bf16x2_f32(w[k]), make_float2(c, c), make_float2(nb, nb));
       s[k & 1] = __fadd2_rn(s[k & 1], make_float2(ex2f_approx(t.x), ex2f_approx(t.y)));
     }
   }
+  // f32 logits: 4 values per 16-byte vector
+  template <int NV>
+  __device__ __forceinline__ void step_f32(const uint8_t* cb, uint32_t v, float c) {
+    float z[4 * NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const uint4 q = lds128(cb + (v + u * kFT) * 16);
+      z[4 * u] = __uint_as_float(q.x); z[4 * u + 1] = __uint_as_float(q.y);
+      z[4 * u + 2] = __uint_as_float(q.z); z[4 * u + 3] = __uint_as_float(q.w);
+    }
+    float lm = fmaxf(z[0], z[1]);
+#pragma unroll
+    for (int k = 2; k < 4 * NV; ++k) lm = fmaxf(lm, z[k]);
+    if (lm > mz) rescale(lm, c);
+#pragma unroll
+    for (int k = 0; k < 2 * NV; ++k) {
+      const float2 t = __ffma2_rn(make_float2(z[2 * k], z[2 * k + 1]), make_float2(c, c), make_float2(nb, nb));
+      s[k & 1] = __fadd2_rn(s[k & 1], make_float2(ex2f_approx(t.x), ex2f_approx(t.y)));
+    }
+  }
+  __device__ __forceinline__ void rescale(float lm, float c) {
+    const float f = ex2f_approx((mz - lm) * c);
+    s[0] = __fmul2_rn(s[0], make_float2(f, f));
+    s[1] = __fmul2_rn(s[1], make_float2(f, f));
+    mz = lm;
+    nb = -mz * c;
+  }
+  template <int DT>
   __device__ __forceinline__ void chunk(const uint8_t* cb, uint32_t bytes, float c, int tid) {
     const uint32_t nv = bytes / 16;
     uint32_t v = tid;
-    for (; v + kFT < nv; v += 2 * kFT) step<2>(cb, v, c);
-    if (v < nv) step<1>(cb, v, c);
+    if constexpr (DT == RLK_BF16) {
+      for (; v + kFT < nv; v += 2 * kFT) step<2>(cb, v, c);
+      if (v < nv) step<1>(cb, v, c);
+    } else {
+      for (; v + kFT < nv; v += 2 * kFT) step_f32<2>(cb, v, c);
+      if (v < nv) step_f32<1>(cb, v, c);
+    }
   }
   __device__ __forceinline__ float sum() const { return (s[0].x + s[0].y) + (s[1].x + s[1].y); }
 };
@@ -169,6 +199,23 @@ __device__ __forceinline__ void grad_step(const uint8_t* cb, uint32_t v, float c
       o[e] = *reinterpret_cast<uint32_t*>(&p2);
     }
     stg128_stream(gout + (uint64_t)(v + u * kFT) * 8, make_uint4(o[0], o[1], o[2], o[3]));
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void grad_step_f32(const uint8_t* cb, uint32_t v, float c, float ncf, float nl, float* gout) {
+#pragma unroll
+  for (int u = 0; u < NV; ++u) {
+    RLK_DCHECK((v + u * kFT) * 16 < kChunkBytes);
+    const uint4 q = lds128(cb + (v + u * kFT) * 16);
+    const float2 t0 = __ffma2_rn(make_float2(__uint_as_float(q.x), __uint_as_float(q.y)), make_float2(c, c),
+                                 make_float2(nl, nl));
+    const float2 t1 = __ffma2_rn(make_float2(__uint_as_float(q.z), __uint_as_float(q.w)), make_float2(c, c),
+                                 make_float2(nl, nl));
+    const float2 g0 = __fmul2_rn(make_float2(ex2f_approx(t0.x), ex2f_approx(t0.y)), make_float2(ncf, ncf));
+    const float2 g1 = __fmul2_rn(make_float2(ex2f_approx(t1.x), ex2f_approx(t1.y)), make_float2(ncf, ncf));
+    stg128_stream(gout + (uint64_t)(v + u * kFT) * 4, make_uint4(__float_as_uint(g0.x), __float_as_uint(g0.y),
+                                                                 __float_as_uint(g1.x), __float_as_uint(g1.y)));
   }
 }
 
@@ -198,14 +245,21 @@ static_assert(896 + 2 * sizeof(RowInfo) <= 1024, "RowInfo must fit the 1 KiB hea
 // epilogue warp (mbarrier), run pass 1 over the chunks of the next row that are already in the ring,
 // and only then wait for row r's coefficient and run its pass 2 -- the cross-CTA exchange and the
 // serial epilogue are off the consumers' critical path.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo_fused_bf16(FusedArgs a) {
+// DT: logits (and gradient) dtype; CL: CTAs per cluster = per row (set at launch).
+template <int DT, int CL>
+__global__ void __launch_bounds__(kFThreads, 1) k_grpo_fused(FusedArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // 1 KiB header: [full[nslots] | empty[nslots] | xbar[2] | pready[2] | cready[2] | ibar[2]] (<= 512 B),
-  // slot[2] float2 @512, bcast[2][4] float @576, red[2][kFW][2] float @640, info[2] RowInfo @896
-  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
-  const uint64_t half = a.vocab / 2;  // elements owned by this CTA (vocab % 16 == 0)
+  // slot[2][CL] float2 @512, bcast[2][4] float @576, red[2][kFW][2] float @640, info[2] RowInfo @896
+  static_assert(2 * CL * 8 <= 64, "peer partial slots overflow the header");
+  constexpr int ESZ = Elem<DT>::size;
+  constexpr uint32_t kCE = kChunkBytes / ESZ;  // elements per chunk
+  constexpr uint32_t kVE = 16 / ESZ;           // elements per 16-byte vector
+  using GT = typename std::conditional<DT == RLK_BF16, uint16_t, float>::type;
+  const uint32_t rank = cluster_rank();
+  const uint64_t half = a.vocab / CL;  // elements owned by this CTA (vocab % (8 CL) == 0)
   const uint64_t v0 = rank * half;
-  const uint32_t half_bytes = (uint32_t)(half * 2);
+  const uint32_t half_bytes = (uint32_t)(half * ESZ);
   const uint32_t nch = (half_bytes + kChunkBytes - 1) / kChunkBytes;  // chunks per half row
   const uint32_t nslots = a.nslots;  // ring slots >= nch: the producer runs ahead into the next row
   const uint32_t pre = min(nch, nslots - nch);  // next-row chunks that fit beside the current row
@@ -248,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       RingPos q;
       for (uint64_t row = row0; row < a.n_rows; row += rstep) {
         if (!active(row)) continue;
-        const char* src = a.logits + (lrow(row) * a.row_stride + v0) * 2;
+        const char* src = a.logits + (lrow(row) * a.row_stride + v0) * ESZ;
         for (uint32_t k = 0; k < nch; ++k) {
           const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
           RLK_DCHECK(q.s < nslots && bytes > 0 && (uint64_t)k * kChunkBytes + bytes <= half_bytes);
@@ -290,13 +344,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       int32_t tok = 0;
       double zt = 0.0, lt64 = 0.0, li64 = 0.0, adv = 0.0, nrm = 0.0;
       if (lane == 0) {
-        mbar_arrive_expect_tx(&xbar[p], 8);  // the peer's partial lands in slot[p]
+        mbar_arrive_expect_tx(&xbar[p], 8 * (CL - 1));  // the peers' partials land in slot[p][r]
         tok = a.tokens[row];
         lt64 = a.lp_train[row];
         li64 = a.lp_infer[row];
         adv = a.adv[s_id];
         nrm = a.norm[s_id];
-        if (tok >= 0 && (uint64_t)tok < a.vocab) zt = load_f64<RLK_BF16>(a.logits + lrow(row) * a.row_stride * 2, (uint64_t)tok);
+        if (tok >= 0 && (uint64_t)tok < a.vocab) zt = load_f64<DT>(a.logits + lrow(row) * a.row_stride * ESZ, (uint64_t)tok);
       }
       mbar_wait(&pready[p], ph[p]);
       float M = -INFINITY, S = 0.f;
@@ -306,18 +360,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       }
       warp_combine(M, S, c);
       if (lane == 0) {
-        RLK_DCHECK(p < 2 && peer < 2);
-        st_async_peer(mapa(smem_u32(&slot[p]), peer), M, S, mapa(smem_u32(&xbar[p]), peer));
+        RLK_DCHECK(p < 2 && rank < (uint32_t)CL);
+#pragma unroll
+        for (uint32_t r = 0; r < (uint32_t)CL; ++r)
+          if (r != rank) st_async_peer(mapa(smem_u32(&slot[p * CL + rank]), r), M, S, mapa(smem_u32(&xbar[p]), r));
         mbar_wait(&xbar[p], ph[p]);
-        const float2 o = slot[p];
         // combine and run the epilogue (objective.py:243-248, 277-279) in float64, like K4's: this
         // warp is off the consumers' critical path, so the precise exp / log cost nothing (an f32
         // epilogue loses ~1e-5 absolute in logp = z/T - lse when |z/T| reaches hundreds).
-        // Both CTAs compute the same numbers; rank 0 writes the per-token outputs.
-        const float Mm = fmaxf(M, o.x);
+        // Every CTA combines the partials in rank order, so all compute the same numbers; rank 0
+        // writes the per-token outputs.
+        float2 part[CL];
+#pragma unroll
+        for (int r = 0; r < CL; ++r) part[r] = (uint32_t)r == rank ? make_float2(M, S) : slot[p * CL + r];
+        float Mm = part[0].x;
+#pragma unroll
+        for (int r = 1; r < CL; ++r) Mm = fmaxf(Mm, part[r].x);
         double Sd = 0.0;
-        if (M != -INFINITY) Sd += (double)S * exp2(((double)M - (double)Mm) * (double)c);
-        if (o.x != -INFINITY) Sd += (double)o.y * exp2(((double)o.x - (double)Mm) * (double)c);
+#pragma unroll
+        for (int r = 0; r < CL; ++r)
+          if (part[r].x != -INFINITY) Sd += (double)part[r].y * exp2(((double)part[r].x - (double)Mm) * (double)c);
         const double lse = (double)Mm / T + log(Sd);  // ln-sum-exp of z / T
         double cf = 0.0;
         if (tok < 0 || (uint64_t)tok >= a.vocab) {
@@ -360,8 +422,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
     uint32_t iph[2] = {0u, 0u};
     // zero the gradient and outputs of inactive rows (objective.py:240-241 / 275-276)
     auto zero_row = [&](uint64_t row) {
-      uint16_t* grow = a.grad + lrow(row) * a.grad_row_stride + v0;
-      for (uint64_t b = (uint64_t)tid * 8; b < half; b += (uint64_t)kFT * 8) stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
+      GT* grow = reinterpret_cast<GT*>(a.grad) + lrow(row) * a.grad_row_stride + v0;
+      for (uint64_t b = (uint64_t)tid * kVE; b < half; b += (uint64_t)kFT * kVE)
+        stg128_stream(grow + b, make_uint4(0, 0, 0, 0));
       if (rank == 0 && tid == 0) {
         if (a.logp) a.logp[row] = 0.0;
         if (a.lse) a.lse[row] = 0.0;
@@ -385,7 +448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       // pass 1 (rest of the row)
       for (uint32_t k = done; k < nch; ++k) {
         mbar_wait(&full[q.s], q.ph);
-        acc.chunk(buf + q.s * kChunkBytes, min(kChunkBytes, half_bytes - k * kChunkBytes), c, tid);
+        acc.chunk<DT>(buf + q.s * kChunkBytes, min(kChunkBytes, half_bytes - k * kChunkBytes), c, tid);
         q.next(nslots);
       }
       float mz = acc.mz, sum = acc.sum();
@@ -408,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
         const float cn = ni.c;
         for (; done < pre; ++done) {
           mbar_wait(&full[q.s], q.ph);
-          acc.chunk(buf + q.s * kChunkBytes, min(kChunkBytes, half_bytes - done * kChunkBytes), cn, tid);
+          acc.chunk<DT>(buf + q.s * kChunkBytes, min(kChunkBytes, half_bytes - done * kChunkBytes), cn, tid);
           q.next(nslots);
         }
       }
@@ -416,31 +479,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
       mbar_wait(&cready[p], cph[p]);
       cph[p] ^= 1u;
       const float cf = bcast[p * 4 + 0], nl = bcast[p * 4 + 1];
-      uint16_t* grow = a.grad + lr * a.grad_row_stride + v0;
+      GT* grow = reinterpret_cast<GT*>(a.grad) + lr * a.grad_row_stride + v0;
       // the chunk / vector / thread that holds the target token's logit (the one-hot term)
       const int64_t tok_local = (int64_t)tok - (int64_t)v0;
       const bool tok_here = tok_local >= 0 && tok_local < (int64_t)half;
-      const uint32_t tok_chunk = tok_here ? (uint32_t)(tok_local / (kChunkBytes / 2)) : 0xffffffffu;
-      const uint32_t tok_vec = tok_here ? (uint32_t)(tok_local % (kChunkBytes / 2)) / 8 : 0u;
+      const uint32_t tok_chunk = tok_here ? (uint32_t)(tok_local / kCE) : 0xffffffffu;
+      const uint32_t tok_vec = tok_here ? (uint32_t)(tok_local % kCE) / kVE : 0u;
       RingPos q2 = q_row;
       for (uint32_t k = 0; k < nch; ++k) {
         const uint32_t bytes = min(kChunkBytes, half_bytes - k * kChunkBytes);
         const uint8_t* cb = buf + q2.s * kChunkBytes;
-        uint16_t* gout = grow + (uint64_t)k * (kChunkBytes / 2);
+        GT* gout = grow + (uint64_t)k * kCE;
         const uint32_t nv = bytes / 16;
         if (cf == 0.f) {  // no gradient for this row (objective.py:277-279 with coef 0)
-          for (uint32_t v = tid; v < nv; v += kFT) stg128_stream(gout + (uint64_t)v * 8, make_uint4(0, 0, 0, 0));
+          for (uint32_t v = tid; v < nv; v += kFT) stg128_stream(gout + (uint64_t)v * kVE, make_uint4(0, 0, 0, 0));
         } else {
           uint32_t v = tid;
-          for (; v + kFT < nv; v += 2 * kFT) grad_step<2>(cb, v, c, -cf, nl, gout);
-          if (v < nv) grad_step<1>(cb, v, c, -cf, nl, gout);
+          if constexpr (DT == RLK_BF16) {
+            for (; v + kFT < nv; v += 2 * kFT) grad_step<2>(cb, v, c, -cf, nl, gout);
+            if (v < nv) grad_step<1>(cb, v, c, -cf, nl, gout);
+          } else {
+            for (; v + kFT < nv; v += 2 * kFT) grad_step_f32<2>(cb, v, c, -cf, nl, gout);
+            if (v < nv) grad_step_f32<1>(cb, v, c, -cf, nl, gout);
+          }
           if (k == tok_chunk && tok_vec % kFT == (uint32_t)tid) {
             // same thread, after its vector store: cf * (1 - softmax) at the target
-            const uint32_t e = (uint32_t)(tok_local % (kChunkBytes / 2));
-            const float z = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(cb)[e] << 16);
+            const uint32_t e = (uint32_t)(tok_local % kCE);
+            float z;
+            if constexpr (DT == RLK_BF16) z = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(cb)[e] << 16);
+            else z = reinterpret_cast<const float*>(cb)[e];
             const float g = cf - cf * ex2f_approx(fmaf(z, c, nl));
-            __nv_bfloat16 hb = __float2bfloat16_rn(g);
-            gout[e] = *reinterpret_cast<uint16_t*>(&hb);
+            if constexpr (DT == RLK_BF16) {
+              __nv_bfloat16 hb = __float2bfloat16_rn(g);
+              gout[e] = *reinterpret_cast<uint16_t*>(&hb);
+            } else {
+              gout[e] = g;
+            }
           }
         }
         __syncwarp();
@@ -455,29 +529,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFThreads, 1) k_grpo
     }
   }
   __syncwarp();
-  cluster_sync_all();  // no CTA leaves while its peer may still st.async into it
+  cluster_sync_all();  // no CTA leaves while its peers may still st.async into it
 }
 
 }  // namespace rlk
 
 using namespace rlk;
 
-extern "C" int rlk_grpo_fused_bf16(const void* logits, uint64_t n_rows, uint64_t vocab, uint64_t row_stride,
-                                   const int64_t* row_index, const int32_t* tokens, const double* logp_train,
-                                   const double* logp_infer, const int32_t* sample_of_row, const double* adv,
-                                   const uint8_t* use, const double* temperature, const double* norm,
-                                   const rlk_clip* clip, double grad_scale, double* logp_out, double* lse_out,
-                                   double* term, double* coef, int32_t* flags, void* grad, uint64_t grad_row_stride,
-                                   void* stream) {
+template <int DT, int CL>
+static int launch_fused(const FusedArgs& a, uint32_t smem, cudaStream_t stream) {
+  auto kern = k_grpo_fused<DT, CL>;
+  if (int st = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                           "cudaFuncSetAttribute"))
+    return st;
+  if (int st = cuda_status(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                           "cudaFuncSetAttribute"))
+    return st;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kFThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent clusters: exactly as many as can be co-resident (a cluster must fit in one GPC, so with
+  // 4-CTA clusters some SMs stay idle -- launching sm_count / CL would leave a second wave of clusters
+  // waiting for whole row sequences of the first)
+  cfg.gridDim = dim3((unsigned)(CL * (sm_count() / CL)), 1, 1);
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters <= 0) {
+    cudaGetLastError();
+    max_clusters = sm_count() / CL;
+  }
+  const uint64_t clusters = std::max<uint64_t>(1, std::min<uint64_t>(a.n_rows, (uint64_t)max_clusters));
+  cfg.gridDim = dim3((unsigned)(CL * clusters), 1, 1);
+  if (int st = cuda_status(cudaLaunchKernelEx(&cfg, kern, a), "cudaLaunchKernelEx")) return st;
+  return launch_status("rlk_grpo_fused");
+}
+
+extern "C" int rlk_grpo_fused(const void* logits, int dtype, uint64_t n_rows, uint64_t vocab, uint64_t row_stride,
+                              const int64_t* row_index, const int32_t* tokens, const double* logp_train,
+                              const double* logp_infer, const int32_t* sample_of_row, const double* adv,
+                              const uint8_t* use, const double* temperature, const double* norm, const rlk_clip* clip,
+                              double grad_scale, double* logp_out, double* lse_out, double* term, double* coef,
+                              int32_t* flags, void* grad, uint64_t grad_row_stride, void* stream) {
   if (n_rows == 0) return RLK_OK;
   RLK_REQUIRE(logits && tokens && logp_train && logp_infer && sample_of_row && adv && use && temperature && norm &&
                   clip && term && coef && flags && grad,
-              "rlk_grpo_fused_bf16: NULL argument");
-  RLK_REQUIRE(vocab % 16 == 0 && vocab * 2 / 2 <= kMaxHalfBytes, "rlk_grpo_fused_bf16: vocab must be a multiple of 16 and <= %u",
-              kMaxHalfBytes);
-  RLK_REQUIRE(row_stride % 8 == 0 && grad_row_stride % 8 == 0 && ((uintptr_t)logits & 15u) == 0 &&
+              "rlk_grpo_fused: NULL argument");
+  RLK_REQUIRE(dtype == RLK_BF16 || dtype == RLK_F32, "rlk_grpo_fused: logits must be bf16 or f32 (got %d)", dtype);
+  const int esz = dtype == RLK_BF16 ? 2 : 4;
+  const int cl = dtype == RLK_BF16 ? 2 : 4;  // CTAs per row: each owns vocab * esz / cl bytes
+  RLK_REQUIRE(vocab % (8 * cl) == 0 && vocab * esz / cl <= kMaxHalfBytes,
+              "rlk_grpo_fused: vocab must be a multiple of %d and at most %u", 8 * cl, kMaxHalfBytes * cl / esz);
+  RLK_REQUIRE(row_stride % (16 / esz) == 0 && grad_row_stride % (16 / esz) == 0 && ((uintptr_t)logits & 15u) == 0 &&
                   ((uintptr_t)grad & 15u) == 0,
-              "rlk_grpo_fused_bf16: rows must be 16-byte aligned");
+              "rlk_grpo_fused: rows must be 16-byte aligned");
   FusedArgs a;
   a.logits = (const char*)logits;
   a.n_rows = n_rows;
@@ -499,16 +610,24 @@ extern "C" int rlk_grpo_fused_bf16(const void* logits, uint64_t n_rows, uint64_t
   a.term = term;
   a.coef = coef;
   a.flags = flags;
-  a.grad = (uint16_t*)grad;
+  a.grad = grad;
   a.grad_row_stride = grad_row_stride;
-  const uint32_t half_bytes = (uint32_t)(vocab);  // vocab/2 elements * 2 bytes
-  const uint32_t nch = (half_bytes + kChunkBytes - 1) / kChunkBytes;
+  const uint32_t part_bytes = (uint32_t)(vocab * esz / cl);
+  const uint32_t nch = (part_bytes + kChunkBytes - 1) / kChunkBytes;
   a.nslots = std::max<uint32_t>(nch, std::min<uint32_t>(60u, (226u * 1024u - 1024u) / kChunkBytes));
   const uint32_t smem = 1024 + a.nslots * kChunkBytes;
-  if (int st = cuda_status(cudaFuncSetAttribute(k_grpo_fused_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)smem), "cudaFuncSetAttribute"))
-    return st;
-  const uint64_t clusters = std::min<uint64_t>((n_rows + 0), (uint64_t)sm_count() / 2);
-  k_grpo_fused_bf16<<<(unsigned)(2 * std::max<uint64_t>(clusters, 1)), kFThreads, smem, (cudaStream_t)stream>>>(a);
-  return launch_status("rlk_grpo_fused_bf16");
+  cudaStream_t s = (cudaStream_t)stream;
+  return dtype == RLK_BF16 ? launch_fused<RLK_BF16, 2>(a, smem, s) : launch_fused<RLK_F32, 4>(a, smem, s);
+}
+
+extern "C" int rlk_grpo_fused_bf16(const void* logits, uint64_t n_rows, uint64_t vocab, uint64_t row_stride,
+                                   const int64_t* row_index, const int32_t* tokens, const double* logp_train,
+                                   const double* logp_infer, const int32_t* sample_of_row, const double* adv,
+                                   const uint8_t* use, const double* temperature, const double* norm,
+                                   const rlk_clip* clip, double grad_scale, double* logp_out, double* lse_out,
+                                   double* term, double* coef, int32_t* flags, void* grad, uint64_t grad_row_stride,
+                                   void* stream) {
+  return rlk_grpo_fused(logits, RLK_BF16, n_rows, vocab, row_stride, row_index, tokens, logp_train, logp_infer,
+                        sample_of_row, adv, use, temperature, norm, clip, grad_scale, logp_out, lse_out, term, coef,
+                        flags, grad, grad_row_stride, stream);
 }

@@ -426,24 +426,33 @@ def grpo_backward(logits: torch.Tensor, batch: GRPOBatch, fwd: GRPOForward, grad
 
 def grpo_forward_backward(logits: torch.Tensor, batch: GRPOBatch, clip: ClipConfig = ClipConfig(),
                           grad_scale: float = 1.0, *, stream=None, group=None) -> tuple[GRPOForward, torch.Tensor]:
-    """J and grad_scale * dJ/dlogits in ONE read of the logits (bf16, one row per token): the fused
-    cluster kernel `rlk_grpo_fused_bf16`.  Other dtypes / layouts fall back to K4 + K5."""
+    """J and grad_scale * dJ/dlogits in ONE read of the logits (bf16 or f32, one row per token): the
+    fused cluster kernel `rlk_grpo_fused` (2-CTA clusters for bf16, 4 for f32); the gradient has the
+    logits' dtype.  f64 logits and `row_index` layouts fall back to K4 + K5."""
     if stream is not None:
         with torch.cuda.stream(stream):
             return grpo_forward_backward(logits, batch, clip, grad_scale, group=group)
     logits = logits.contiguous()
     R, V = logits.shape
-    if logits.dtype != torch.bfloat16 or batch.row_index is not None or V % 16 or V > 204800:
+    cl = 2 if logits.dtype == torch.bfloat16 else 4
+    if logits.dtype not in (torch.bfloat16, torch.float32) or batch.row_index is not None or V % (8 * cl) \
+            or V > 204800:
         fwd = grpo_forward(logits, batch, clip, group=group)
         return fwd, grpo_backward(logits, batch, fwd, grad_scale, group=group)
+    nb = batch.n_rows  # token r reads logits row r; rows past the batch get a zero gradient
+    if nb > R:
+        raise ValueError(f"batch has {nb} token rows but logits only {R}")
     dev = logits.device
     f64 = dict(dtype=torch.float64, device=dev)
-    logp, lse, term, coef = (torch.empty(R, **f64) for _ in range(4))
+    logp, lse, term, coef = (torch.empty(nb, **f64) for _ in range(4))
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     grad = torch.empty_like(logits)
+    if nb < R:
+        grad[nb:].zero_()
     c = clip.c_struct()
     s = L.stream_handle()
-    L.call("rlk_grpo_fused_bf16", L.ptr(logits), R, V, V, None, L.ptr(batch.tokens), L.ptr(batch.logp_train),
+    L.call("rlk_grpo_fused", L.ptr(logits), L.dtype_code(logits.dtype), nb, V, V, None, L.ptr(batch.tokens),
+           L.ptr(batch.logp_train),
            L.ptr(batch.logp_infer), L.ptr(batch.sample_of_row), L.ptr(batch.adv), L.ptr(batch.use),
            L.ptr(batch.temperature), L.ptr(batch.norm), L.C.byref(c), float(grad_scale), L.ptr(logp), L.ptr(lse),
            L.ptr(term), L.ptr(coef), L.ptr(flags), L.ptr(grad), V, s)

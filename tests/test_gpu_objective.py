@@ -201,6 +201,23 @@ def test_fused_forward_backward(cuda, V):
     logits, toks, lt, li, adv, use, cu = _synthetic_rows(Rps, S, V, G, seed=3, tau=0.8, masked=(2, 5))
     b = O.GRPOBatch.pack(toks, lt, li, cu, adv, use, G, T_max, temperature=0.8, device=cuda)
     lg = torch.from_numpy(logits).to(cuda, torch.bfloat16)
+    _fused_vs_k4k5(O, lg, b, logits, toks, use, S, Rps, V, 2.0 ** -8 + 1e-5, "bf16")
+
+
+@pytest.mark.parametrize("V", [131072, 4096, 204800])
+def test_fused_forward_backward_f32(cuda, V):
+    """f32 logits: the 4-CTA-cluster one-read kernel == K4 + K5, f32 gradient pinned per element."""
+    from paper_2509_18883_b200 import objective as O
+    G, S, Rps, T_max = 4, 8, 9, 16
+    logits, toks, lt, li, adv, use, cu = _synthetic_rows(Rps, S, V, G, seed=4, tau=0.8, masked=(1, 6))
+    g = np.random.default_rng(9)
+    logits = (logits + g.normal(0, 1e-3, logits.shape)).astype(np.float32).astype(np.float64)  # not bf16-valued
+    b = O.GRPOBatch.pack(toks, lt, li, cu, adv, use, G, T_max, temperature=0.8, device=cuda)
+    lg = torch.from_numpy(logits).to(cuda, torch.float32)
+    _fused_vs_k4k5(O, lg, b, logits, toks, use, S, Rps, V, 5e-6, "f32")
+
+
+def _fused_vs_k4k5(O, lg, b, logits, toks, use, S, Rps, V, rtol, tag):
     fwd, grad = O.grpo_forward_backward(lg, b, grad_scale=-1.0)
     ref = O.grpo_forward(lg, b)
     gref = O.grpo_backward(lg, b, ref, -1.0, grad_dtype=torch.float32)
@@ -208,15 +225,16 @@ def test_fused_forward_backward(cuda, V):
     assert float(fwd.objective) == pytest.approx(float(ref.objective), rel=2e-6, abs=1e-12)
     np.testing.assert_allclose(fwd.logp.cpu().numpy(), ref.logp.cpu().numpy(), rtol=0, atol=2e-6)
     np.testing.assert_allclose(fwd.coef.cpu().numpy(), ref.coef.cpu().numpy(), rtol=2e-6, atol=1e-12)
-    # every entry of the one-read bf16 gradient vs grad_scale * coef * (onehot - softmax) in f64
+    # every entry of the one-read gradient vs grad_scale * coef * (onehot - softmax) in f64
+    assert grad.dtype == lg.dtype
     cf = -fwd.coef.cpu().numpy()
-    worst = assert_grad_rows(grad.double().cpu().numpy(), logits, toks, cf, [0.8] * len(toks), 2.0 ** -8 + 1e-5)
-    print(f"fused bf16 grad V={V}: worst per-element error = {worst:.3f} of the bound")
+    worst = assert_grad_rows(grad.double().cpu().numpy(), logits, toks, cf, [0.8] * len(toks), rtol)
+    print(f"fused {tag} grad V={V}: worst per-element error = {worst:.3f} of the bound")
     # and against K5's f32 gradient: both within bf16 rounding of each other
     g32 = gref.cpu().numpy()
     assert_grad_rows(g32, logits, toks, cf, [0.8] * len(toks), 1e-5)
     sor = np.repeat(np.arange(S), Rps)
-    assert not grad[torch.from_numpy(~use[sor].astype(bool)).to(cuda)].any()
+    assert not grad[torch.from_numpy(~use[sor].astype(bool)).to(lg.device)].any()
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
@@ -244,7 +262,7 @@ def test_extreme_logits_vs_oracle(cuda, dtype):
                                           [1.0, -1.0], [1, 1], [tau, tau], clip, norm=1.0 / (2 * R))
         np.testing.assert_allclose(fwd.logp.cpu().numpy(), logp, rtol=1e-6, atol=1e-5)
         np.testing.assert_allclose(fwd.term.cpu().numpy(), term, rtol=1e-4, atol=1e-9)
-        if dtype == torch.bfloat16:
+        if True:  # the one-read kernel for both dtypes (2- and 4-CTA clusters)
             fused, grad = O.grpo_forward_backward(lg, b)
             assert int(fused.flags.item()) == 0
             assert float(fused.objective) == pytest.approx(float(fwd.objective), rel=1e-4, abs=1e-9)
