@@ -118,7 +118,50 @@ def check(status: int, where: str = "") -> None:
 
 
 def call(name: str, *args) -> None:
-    check(getattr(lib(), name)(*args), name)
+    """One C-ABI entry point, inside an NVTX range of its name (visible in Nsight timelines; a no-op
+    marker without a profiler attached)."""
+    nv = _nvtx()
+    if nv is None:
+        check(getattr(lib(), name)(*args), name)
+        return
+    nv.range_push(name)
+    try:
+        check(getattr(lib(), name)(*args), name)
+    finally:
+        nv.range_pop()
+
+
+_NVTX = None
+
+
+def _nvtx():
+    global _NVTX
+    if _NVTX is None:
+        try:
+            import torch
+            _NVTX = torch.cuda.nvtx if torch.cuda.is_available() else False
+        except Exception:  # pragma: no cover - torch without CUDA
+            _NVTX = False
+    return _NVTX or None
+
+
+class nvtx_range:
+    """`with nvtx_range("rlk.fusion_step"):` -- an NVTX range around a multi-kernel step."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        nv = _nvtx()
+        if nv is not None:
+            nv.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        nv = _nvtx()
+        if nv is not None:
+            nv.range_pop()
+        return False
 
 
 def dtype_code(dtype) -> int:

@@ -313,9 +313,9 @@ class FusionCall:
     def run(self, weights: Sequence[float], dtype_out: torch.dtype | None = None) -> "FusionCall":
         """One complete fusion step on the call's stream: zero counters, [K2], K1, [all_reduce],
         finalize, K3.  Reusing a FusionCall across steps reuses its launch plan (host metadata only)."""
-        with torch.cuda.stream(self.stream):
+        with L.nvtx_range("rlk.fusion_step"), torch.cuda.stream(self.stream):
             self.counters.zero_()
-        return self.norms().merge(weights, dtype_out)
+            return self.norms().merge(weights, dtype_out)
 
     def capture(self, weights: Sequence[float], dtype_out: torch.dtype | None = None) -> "torch.cuda.CUDAGraph":
         """`run(weights)` captured once into a CUDA graph on the call's stream; `graph.replay()` inside

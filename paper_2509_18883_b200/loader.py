@@ -323,7 +323,8 @@ def fuse_streaming(names: Sequence[str], numels: Sequence[int], n_experts: int, 
             ready = torch.cuda.Event()
             ready.record(h2d_s)
             comp_s.wait_event(ready)
-            call.run(weights)
+            with L.nvtx_range(f"rlk.stream_group.{gi}"):
+                call.run(weights)
             done = torch.cuda.Event()
             done.record(comp_s)
             # drain the previous group while this one computes
