@@ -104,11 +104,19 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return rank, world, local, None
+    # RLK_BENCH_BACKEND=gloo runs the N > 1 code path with every rank on the visible GPUs round-robin
+    # (a functional check of the sharded bench on a one-GPU box; NCCL refuses two ranks per GPU).
+    backend = os.environ.get("RLK_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
     return rank, world, local, group
 
