@@ -15,6 +15,7 @@
  *   rlk_fusion_mask_bitmap_range  (the same, one index slice)       fusion.py:105-115
  *   rlk_fusion_merge        dropout_prune rescale, erase_minority,   fusion.py:114, 118-142
  *                           fuse weighted sum + FusionStats counts   fusion.py:154-188
+ *   rlk_fusion_merge_ws     (the same, with a fix-up workspace)      fusion.py:114-188
  *   rlk_grpo_fwd            log_token_dist + objective_value         toy_env.py:157-175, objective.py:230-250
  *                           (tis_weight, _triplet_value_slope)       objective.py:133-165
  *   rlk_segment_sum_f64     per-group token-term sums                objective.py:238-250
@@ -121,6 +122,19 @@ int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, i
                      const uint64_t* child_seeds, uint64_t thresh, double keep_prob,
                      const uint32_t* bitmap, uint64_t words_per_row, int erase_mode,
                      unsigned long long* counters, int exact_path, void* stream);
+
+/* rlk_fusion_merge with a caller workspace for the bf16 fast path: elements whose certified f32
+ * evaluation is inconclusive (~0.05% with normalisation) are queued per CTA and finished by a fix-up
+ * kernel on the same stream (reference-order float64, one element per thread) instead of by one lane
+ * of a warp inside the merge.  workspace: 16-byte aligned device memory, RLK_MERGE_WS_HEADER bytes of
+ * queue lengths + 8 bytes per queued element (a full queue falls back to the in-kernel path); NULL or 0
+ * = rlk_fusion_merge.  Results are identical either way. */
+#define RLK_MERGE_WS_HEADER 4096
+int rlk_fusion_merge_ws(const rlk_fusion_plan* plan, int n_experts, int dtype_in, int dtype_out, int delta_mode,
+                        const double* scale, const double* weights, int dropout_mode, const uint64_t* child_seeds,
+                        uint64_t thresh, double keep_prob, const uint32_t* bitmap, uint64_t words_per_row,
+                        int erase_mode, unsigned long long* counters, int exact_path, void* workspace,
+                        uint64_t workspace_bytes, void* stream);
 
 /* GRPO token objective over packed rows (K4).  Token r reads logits row row_index[r] (or r when
  * row_index is NULL), row_stride elements between rows, vocab V.  Per token: token id, behaviour

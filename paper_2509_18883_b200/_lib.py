@@ -17,6 +17,7 @@ RLK_ERR_CUDA = -2
 RLK_ERR_UNSUPPORTED = -3
 
 RLK_BF16, RLK_F32, RLK_F64 = 0, 1, 2
+RLK_MERGE_WS_HEADER = 4096  # include/rlk.h
 RLK_MAX_EXPERTS = 8
 RLK_FUSION_ITEM = 65536
 
@@ -56,6 +57,8 @@ SIGNATURES = {
     "rlk_fusion_mask_bitmap_range": (_I, [_P, _I, _U64, _U64, _U64, _P, _U64, _P]),
     "rlk_fusion_merge": (_I, [C.POINTER(FusionPlanC), _I, _I, _I, _I, _P, _P, _I, _P, _U64, _D, _P, _U64, _I,
                               _P, _I, _P]),
+    "rlk_fusion_merge_ws": (_I, [C.POINTER(FusionPlanC), _I, _I, _I, _I, _P, _P, _I, _P, _U64, _D, _P, _U64, _I,
+                                 _P, _I, _P, _U64, _P]),
     "rlk_grpo_fwd": (_I, [_P, _I, _U64, _U64, _U64, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.POINTER(ClipC), _P, _P,
                           _P, _P, _P, _P, _U64, _P]),
     "rlk_segment_sum_f64": (_I, [_P, _P, _U64, _P, _P]),

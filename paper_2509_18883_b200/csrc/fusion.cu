@@ -567,6 +567,12 @@ struct MergeArgs {
   uint32_t stage_bytes, nstages;
   const uint32_t* bitmap;
   uint32_t sub_shift;  // K3 work unit = 1 / 2^sub_shift of an item (small layouts: more CTAs busy)
+  // deferred exact path of the bf16 fast merge: per CTA a queue of flagged elements (segment, element)
+  // and its length, finished by k_merge_fixup after the merge (null: exact path inside the merge)
+  uint2* fix_q;
+  uint32_t* fix_count;
+  uint32_t fix_cap;        // entries per CTA (set at launch from the total)
+  uint64_t fix_cap_total;  // entries in the caller's workspace
 };
 
 struct ElemConsts {
@@ -687,9 +693,8 @@ __device__ __forceinline__ uint32_t fast_opp_bits(float b, const float* x, uint3
   return m;
 }
 
-// Phase-2 resolver: one flagged element re-evaluated in scalar f32 -- the fast path's certification
-// is per pair (a failed vote margin flags both elements), so most flagged elements are certifiable on
-// their own.  ERASE 0 / 1 only (the squared vote keeps the f64 path).  Returns
+// Phase-2 resolver: one flagged element re-evaluated in scalar f32 (exact ties, and elements flagged by
+// a margin the scalar re-check can still certify).  ERASE 0 / 1 only (the squared vote keeps the f64 path).  Returns
 //   1: certified like the fast path (same vote-sign and output-bracket arguments); the fast loop's
 //      erased count for this element stands;
 //   2: an exact sum-vote tie, certified: with every scale an exact power of two and no dropout or a
@@ -992,6 +997,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
   constexpr uint32_t ELEMS = SB / 2;
   constexpr uint32_t BMB = ELEMS / 8;
   constexpr bool kErase = (ERASE != 0) && (N >= 2);
+  __shared__ uint32_t fix_n;  // flagged elements this CTA queued for k_merge_fixup
+#ifdef RLK_DEBUG_FLAGS
+  uint32_t dbg_vote = 0, dbg_brk = 0;
+#endif
+  if (threadIdx.x == 0) fix_n = 0;
   const Ring r = ring_setup(smem, a.stage_bytes, a.nstages, kFastCWarps);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kFastCWarps) {
@@ -1104,7 +1114,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         }
         uint32_t outw[kFastPairs];
         uint32_t mx[kFastPairs];  // bf16x2(y - margin) ^ bf16x2(y + margin): non-zero half -> recompute
-        float gm[kFastPairs];     // vote / overflow margin per pair: < 0 (or NaN) -> recompute both
+        float2 gm[kFastPairs];    // vote / overflow margin per element: < 0 (or NaN) -> recompute it
 #pragma unroll
         for (int p = 0; p < kFastPairs; ++p) {
           const uint32_t bw = bw4.w[p];
@@ -1212,15 +1222,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
             // with sr >= 2^-16; g3 = max(S * 2^38 - 1, -S) < 0 exactly for 0 < S < 2^-38 (-0 for S == 0,
             // an all-zero column), and overflow to inf makes a margin NaN
             const float2 g3a = __ffma2_rn(S2, make_float2(0x1p38f, 0x1p38f), make_float2(-1.f, -1.f));
-            gm[p] = fmin_nan(fmin3_nan(g1.x, g1.y, fmaxf(g3a.x, -S2.x)), fmaxf(g3a.y, -S2.y));
+            gm[p] = make_float2(fmin_nan(g1.x, fmaxf(g3a.x, -S2.x)), fmin_nan(g1.y, fmaxf(g3a.y, -S2.y)));
           } else {
-            gm[p] = fmin_nan(g1.x, g1.y);
+            gm[p] = g1;
           }
           outw[p] = wlo;
         }
-        float gmin = gm[0];
+        float gmin = fmin_nan(gm[0].x, gm[0].y);
 #pragma unroll
-        for (int q = 1; q < kFastPairs; ++q) gmin = fmin_nan(gmin, gm[q]);
+        for (int q = 1; q < kFastPairs; ++q) gmin = fmin3_nan(gmin, gm[q].x, gm[q].y);
         uint32_t anym = mx[0];
 #pragma unroll
         for (int q = 1; q < kFastPairs; ++q) anym |= mx[q];
@@ -1228,8 +1238,14 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
           uint32_t slowm = 0;
 #pragma unroll
           for (int q = 0; q < kFastPairs; ++q) {
-            const uint32_t bad = !(gm[q] >= 0.f);
-            slowm |= ((bad | ((mx[q] & 0xffffu) != 0u)) << (2 * q)) | ((bad | ((mx[q] >> 16) != 0u)) << (2 * q + 1));
+            // per element: a failed vote margin flags only its own element (its pair partner's
+            // margin and bracket are independent)
+            const uint32_t bad_x = !(gm[q].x >= 0.f), bad_y = !(gm[q].y >= 0.f);
+#ifdef RLK_DEBUG_FLAGS
+            dbg_vote += bad_x + bad_y;
+            dbg_brk += ((mx[q] & 0xffffu) != 0u) + ((mx[q] >> 16) != 0u);
+#endif
+            slowm |= ((bad_x | ((mx[q] & 0xffffu) != 0u)) << (2 * q)) | ((bad_y | ((mx[q] >> 16) != 0u)) << (2 * q + 1));
           }
           slowbits |= slowm << jit;
         }
@@ -1245,6 +1261,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         uint32_t jit = 0;
         for (uint32_t v = tid; v < nvec; v += kFastCThreads, jit += kFastElems) vec(v, jit);
       }
+#ifdef RLK_TIMING_SKIP_PHASE2  // diagnostic builds only (tools/build_variant.py): phase 2 not run
+      slowbits = 0;
+#endif
       // phase 2 (rare): exact reference-order evaluation of the recorded elements, read back from the
       // stage; the 2-byte store follows this thread's own vector store of the same word
       while (slowbits) {
@@ -1260,19 +1279,30 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
           xe.v[i] = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le] << 16);
           keep |= DROP ? (((uint32_t)bm[i * BMB + (le >> 3)] >> (le & 7)) & 1u) << i : (1u << i);
         }
-        if constexpr (ERASE != 2) {
-          uint32_t xb[N], fo = 0;
-          uint16_t wout;
+        if constexpr (ERASE == 1) {
+          if (tie_ok) {  // exact sum-vote ties certified in scalar f32 (the common flag without normalisation)
+            uint32_t xb[N], fo = 0;
+            uint16_t wout;
 #pragma unroll
-          for (int i = 0; i < N; ++i) xb[i] = reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le];
-          const int kind = scalar_resolve<N, ERASE, UNI>(reinterpret_cast<const uint16_t*>(sb)[le], xb, keep, sr32,
-                                                         w32, wh32, wmax, tie_ok, &wout, &fo);
-          if (kind) {
-            if (kind == 2) {
+            for (int i = 0; i < N; ++i) xb[i] = reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le];
+            const int kind = scalar_resolve<N, ERASE, UNI>(reinterpret_cast<const uint16_t*>(sb)[le], xb, keep,
+                                                           sr32, w32, wh32, wmax, tie_ok, &wout, &fo);
+            if (kind) {
+              if (kind == 2) {
 #pragma unroll
-              for (int i = 0; i < N; ++i) cnt_er[i] -= (fo >> i) & 1u;
+                for (int i = 0; i < N; ++i) cnt_er[i] -= (fo >> i) & 1u;
+              }
+              outp[out_base + le] = wout;
+              continue;
             }
-            outp[out_base + le] = wout;
+          }
+        }
+        if (a.fix_q) {
+          // defer to k_merge_fixup: one warp lane here would hold 31 idle lanes for the whole f64
+          // evaluation; the fix-up kernel runs the queued elements one per thread
+          const uint32_t slot = atomicAdd(&fix_n, 1u);
+          if (slot < a.fix_cap) {
+            a.fix_q[(uint64_t)blockIdx.x * a.fix_cap + slot] = make_uint2(cur.lo, (uint32_t)(out_base + le));
             continue;
           }
         }
@@ -1314,6 +1344,62 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
     for (int i = 0; i < N; ++i) {
       const uint32_t er = __reduce_add_sync(0xffffffffu, cnt_er[i]);
       if (lane == 0 && er) atomicAdd(a.counters + (uint64_t)g.tensor * 2 * N + N + i, (unsigned long long)er);
+    }
+  }
+#ifdef RLK_DEBUG_FLAGS
+  {
+    const uint32_t v = __reduce_add_sync(0xffffffffu, dbg_vote), b = __reduce_add_sync(0xffffffffu, dbg_brk);
+    if (lane == 0 && blockIdx.x < 4) printf("DBG blk %d warp %d vote %u bracket %u\n", (int)blockIdx.x, warp, v, b);
+  }
+#endif
+  if (a.fix_q) {
+    asm volatile("bar.sync 2, %0;" ::"n"(kFastCThreads) : "memory");  // every consumer warp has queued
+    if (tid == 0) a.fix_count[blockIdx.x] = min(fix_n, a.fix_cap);
+  }
+}
+
+// Deferred exact path of k_merge_fast: block b finishes the elements merge CTA b queued, one per thread,
+// from global memory in the reference's operation order (merge_elem_f64), and replaces the fast loop's
+// erased counts for them (fast_opp_bits -> exact).  Same stream, right after the merge.
+template <int N, int DROP, int ERASE>
+__global__ void __launch_bounds__(256) k_merge_fixup(const __grid_constant__ MergeArgs a) {
+  constexpr bool kErase = (ERASE != 0) && (N >= 2);
+  constexpr float kKS = ERASE == 2 ? 1.f : 0x1p24f;  // the fast kernel's scaled domain (sr32 for fast_opp_bits)
+  const uint32_t n = a.fix_count[blockIdx.x];
+  for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const uint2 e = a.fix_q[(uint64_t)blockIdx.x * a.fix_cap + k];
+    const rlk_fusion_segment* seg = a.plan.segs + e.x;
+    const uint64_t idx = e.y;
+    const uint32_t t = seg->tensor;
+    ElemConsts c;
+    float sr32[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      c.scale[i] = a.scale[(uint64_t)t * N + i];
+      sr32[i] = (float)(DROP ? c.scale[i] / a.keep_prob : c.scale[i]) * kKS;
+    }
+    const uint16_t bb = reinterpret_cast<const uint16_t*>(seg->base)[idx];
+    float xf[N];
+    double X[N];
+    uint32_t keep = 0;
+    const uint64_t j = seg->j0 + idx;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      xf[i] = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(seg->expert[i])[idx] << 16);
+      X[i] = (double)xf[i];
+      keep |= (DROP ? ((a.bitmap[(uint64_t)i * a.words_per_row + (j >> 5)] >> (j & 31)) & 1u) : 1u) << i;
+    }
+    const float bf = __uint_as_float((uint32_t)bb << 16);
+    uint32_t nzm, erm;
+    const double Y = merge_elem_f64<N>((double)bf, X, keep, a, c, nzm, erm);
+    reinterpret_cast<uint16_t*>(seg->out)[idx] = f64_to_bf16_rne(Y);
+    if constexpr (kErase) {
+      const uint32_t fo = fast_opp_bits<N>(bf, xf, keep, sr32, ERASE, false);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int corr = (int)((erm >> i) & 1u) - (int)((fo >> i) & 1u);
+        if (corr) atomicAdd(a.counters + (uint64_t)t * 2 * N + N + i, (unsigned long long)(long long)corr);
+      }
     }
   }
 }
@@ -1379,8 +1465,17 @@ static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
   const uint32_t cap = kFastCtas * (uint32_t)sm_count();
   a.sub_shift = sub_shift_for(a.plan.n_items, cap, kItem / kFastSB * 2);
   uint32_t grid = std::min<uint32_t>(a.plan.n_items << a.sub_shift, cap);
+  if (a.fix_q) {
+    a.fix_cap = (uint32_t)std::min<uint64_t>(a.fix_cap_total / grid, 0xffffffffu);
+    if (a.fix_cap == 0) a.fix_q = nullptr;
+  }
   kern<<<grid, kFastThreads, smem, s>>>(a);
-  return launch_status("rlk_fusion_merge");
+  if (int st = launch_status("rlk_fusion_merge")) return st;
+  if (a.fix_q) {
+    k_merge_fixup<N, DROP, ERASE><<<grid, 256, 0, s>>>(a);
+    return launch_status("rlk_fusion_merge (fix-up)");
+  }
+  return RLK_OK;
 }
 
 template <int N>
@@ -1547,6 +1642,16 @@ int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, i
                      const double* scale, const double* weights, int dropout_mode, const uint64_t* child_seeds,
                      uint64_t thresh, double keep_prob, const uint32_t* bitmap, uint64_t words_per_row,
                      int erase_mode, unsigned long long* counters, int exact_path, void* stream) {
+  return rlk_fusion_merge_ws(plan, n_experts, dtype_in, dtype_out, delta_mode, scale, weights, dropout_mode,
+                             child_seeds, thresh, keep_prob, bitmap, words_per_row, erase_mode, counters, exact_path,
+                             nullptr, 0, stream);
+}
+
+int rlk_fusion_merge_ws(const rlk_fusion_plan* plan, int n_experts, int dtype_in, int dtype_out, int delta_mode,
+                        const double* scale, const double* weights, int dropout_mode, const uint64_t* child_seeds,
+                        uint64_t thresh, double keep_prob, const uint32_t* bitmap, uint64_t words_per_row,
+                        int erase_mode, unsigned long long* counters, int exact_path, void* workspace,
+                        uint64_t workspace_bytes, void* stream) {
   RLK_REQUIRE(plan && scale && weights && counters, "rlk_fusion_merge: NULL argument");
   RLK_REQUIRE(n_experts >= 1 && n_experts <= RLK_MAX_EXPERTS, "rlk_fusion_merge: bad expert count %d", n_experts);
   RLK_REQUIRE(dropout_mode >= 0 && dropout_mode <= 2, "rlk_fusion_merge: bad dropout mode %d", dropout_mode);
@@ -1575,6 +1680,12 @@ int rlk_fusion_merge(const rlk_fusion_plan* plan, int n_experts, int dtype_in, i
   a.delta_mode = delta_mode & 1;
   a.with_base = (delta_mode & 1) ? ((delta_mode >> 1) & 1) : 1;
   a.fast = exact_path ? 0 : 1;
+  // workspace: [per-CTA queue lengths: 4 KiB | queue entries (8 B each)]
+  if (workspace && workspace_bytes > RLK_MERGE_WS_HEADER && ((uintptr_t)workspace & 15u) == 0) {
+    a.fix_count = (uint32_t*)workspace;
+    a.fix_q = (uint2*)((char*)workspace + RLK_MERGE_WS_HEADER);
+    a.fix_cap_total = (workspace_bytes - RLK_MERGE_WS_HEADER) / sizeof(uint2);
+  }
   cudaStream_t s = (cudaStream_t)stream;
   switch (dtype_in) {
     case RLK_BF16: return dispatch_merge_out<RLK_BF16>(dtype_out, n_experts, a, s);
