@@ -769,7 +769,8 @@ __device__ __forceinline__ int scalar_resolve(uint32_t bbits, const uint32_t* xb
     for (int i = 0; i < N; ++i) y = fmaf(w32[i], k[i], y);
   }
   if (!(fabsf(y) < INFINITY)) return 0;
-  const uint16_t lo = f32_to_bf16_rne(fmaf(-0x1p-20f, S, y)), hi = f32_to_bf16_rne(fmaf(0x1p-20f, S, y));
+  constexpr float kBr = (float)(N + 7) * 0x1p-24f;  // the fast path's bracket (its error bound covers both kinds)
+  const uint16_t lo = f32_to_bf16_rne(fmaf(-kBr, S, y)), hi = f32_to_bf16_rne(fmaf(kBr, S, y));
   if (lo != hi) return 0;
   *out = lo;
   return kind;
@@ -1015,6 +1016,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
   const uint32_t nib_mask = (tid & 1) ? 0xf0u : 0x0fu;
   const uint32_t nib_mul = (tid & 1) ? 0x01020408u : 0x10204080u;
   const float cv = ERASE == 1 ? 0x1p-20f : 0x1p-19f;
+  constexpr float kBr = (float)(N + 7) * 0x1p-24f;  // output bracket half-width / S (see the bound below)
   // Scaled domain (ERASE 0 / 1): the kernel works with k' = k * 2^24 and folds 2^-24 into the weights
   // (both exact power-of-two scalings).  Every non-zero k' is then a normal float (|d| >= 2^-133,
   // sr >= 2^-16), so its rounding error is relative, and the vote's partial sums are either normal or
@@ -1101,7 +1103,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         // product are ignored), PRMT sign-replication turns them into halfword masks, and one LOP3 per
         // word swaps every dropped expert half for the base half, so d = x - b is exactly +0 there
         // (reference: k = 0, fusion.py:114)
-        static_assert(N <= 8, "output guard certified for N <= 10");
+        static_assert(N <= 8, "the output bracket constant is derived for N <= 8 (RLK_MAX_EXPERTS)");
         uint32_t spread[N][(kFastElems + 3) / 4];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
@@ -1206,15 +1208,17 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
             // below cannot see (a NaN y rounds both bracket ends to the same word)
             g1 = __fmul2_rn(y2, make_float2(0.f, 0.f));
           }
-          // bf16 rounding must be certain.  The f32 evaluation error is <= (4 + N + 1) * 2^-24 * S with
-          // S = |b| + max w * sum|k| (3 roundings in k, 1 in w, N in the weighted sum, 1 in y), so the
-          // reference's value lies in [y - 2^-20 S, y + 2^-20 S] (the two bracket ends are rounded once
-          // each, losing at most 2^-24 S of the 16 * 2^-24 S margin: certified for N <= 10).  RN to bf16 is
-          // monotone, so if both ends round to the same bf16 word, so does the reference's value -- the
-          // bracket covers the rounding boundaries on both sides of y, including the closer one below a
-          // power of two.  The output IS the lower end's word.
-          const float2 ylo = __ffma2_rn(make_float2(-0x1p-20f, -0x1p-20f), S2, y2);
-          const float2 yhi = __ffma2_rn(make_float2(0x1p-20f, 0x1p-20f), S2, y2);
+          // bf16 rounding must be certain.  The f32 evaluation error is <= (N + 5) * 2^-24 * S with
+          // S = |b| + max w * sum|k|: 3 roundings in k, 1 in w, 1 in y, and N more -- the weighted sum
+          // (N roundings, general weights), or for uniform weights (N - 1)/2 each from sum|k| and sum k
+          // (weighted by w/2) plus 1 for sg sum|k| + sum k.  So the reference's value lies in
+          // [y - c S, y + c S] with c = (N + 7) 2^-24: one 2^-24 S for the rounding of each bracket end
+          // (|end| <= (1 + c) S) and one spare (S2 itself is computed short by <= N 2^-24 relative).  RN to
+          // bf16 is monotone, so if both ends round to the same bf16 word, so does the reference's value
+          // -- the bracket covers the rounding boundaries on both sides of y, including the closer one
+          // below a power of two.  The output IS the lower end's word.
+          const float2 ylo = __ffma2_rn(make_float2(-kBr, -kBr), S2, y2);
+          const float2 yhi = __ffma2_rn(make_float2(kBr, kBr), S2, y2);
           const uint32_t wlo = pack_bf16x2(ylo);
           mx[p] = wlo ^ pack_bf16x2(yhi);
           if constexpr (ERASE == 2) {
