@@ -231,6 +231,7 @@ def fusion_bench(args, rank, world, local, group):
     # per-step kernel time (a sharded K2 may be several range launches per step)
     kern = {name: sum(a.elapsed_time(b) for a, b in evs) / nprof for name, evs in call.timers.items()}
     launches = sum(len(evs) for evs in call.timers.values()) // nprof
+    launches += 1 if getattr(call, "_ws", None) is not None else 0  # rlk_fusion_merge_ws: merge + fix-up kernel
     call.timers = None
     ms_max, = max_over_ranks([ms], group)
     kmax = dict(zip(kern.keys(), max_over_ranks(list(kern.values()), group)))
