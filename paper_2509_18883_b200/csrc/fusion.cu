@@ -569,7 +569,7 @@ struct MergeArgs {
   uint32_t sub_shift;  // K3 work unit = 1 / 2^sub_shift of an item (small layouts: more CTAs busy)
   // deferred exact path of the bf16 fast merge: per CTA a queue of flagged elements (segment, element)
   // and its length, finished by k_merge_fixup after the merge (null: exact path inside the merge)
-  uint2* fix_q;
+  uint4* fix_q;  // entries of kFixWords<N> uint4: segment | keep << 24, element, the bf16 inputs
   uint32_t* fix_count;
   uint32_t fix_cap;        // entries per CTA (set at launch from the total)
   uint64_t fix_cap_total;  // entries in the caller's workspace
@@ -578,6 +578,10 @@ struct MergeArgs {
 struct ElemConsts {
   double scale[RLK_MAX_EXPERTS];
 };
+
+// uint4 words per fix-up queue entry: segment | keep << 24, element, then 1 + N bf16 inputs
+template <int N> constexpr int kFixWords = N <= 3 ? 1 : 2;
+static_assert(RLK_MAX_EXPERTS <= 8, "a fix-up entry holds at most 9 bf16 inputs and 8 keep bits");
 
 // RN(a / b) from r = RN(1/b): q = RN(a r); e = a - q b (exact by FMA); RN(q + e r) (Markstein).
 __device__ __forceinline__ double div_rn(double a, double b, double r) {
@@ -1303,10 +1307,24 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
         }
         if (a.fix_q) {
           // defer to k_merge_fixup: one warp lane here would hold 31 idle lanes for the whole f64
-          // evaluation; the fix-up kernel runs the queued elements one per thread
+          // evaluation; the fix-up kernel runs the queued elements one per thread.  The entry carries
+          // the keep bits and the bf16 inputs (from the stage), so the fix-up reads no parameters.
           const uint32_t slot = atomicAdd(&fix_n, 1u);
           if (slot < a.fix_cap) {
-            a.fix_q[(uint64_t)blockIdx.x * a.fix_cap + slot] = make_uint2(cur.lo, (uint32_t)(out_base + le));
+            uint32_t h[2 + N];
+            h[0] = reinterpret_cast<const uint16_t*>(sb)[le];
+#pragma unroll
+            for (int i = 0; i < N; ++i) h[1 + i] = reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le];
+            h[1 + N] = 0;
+            uint4* q = a.fix_q + ((uint64_t)blockIdx.x * a.fix_cap + slot) * kFixWords<N>;
+            q[0] = make_uint4(cur.lo | (keep << 24), (uint32_t)(out_base + le), h[0] | (h[1] << 16),
+                              N >= 2 ? (h[2] | (h[3] << 16)) : 0u);
+            if constexpr (kFixWords<N> > 1) {
+              uint32_t r[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int k = 4; k < 2 + N; k += 2) r[(k - 4) / 2] = h[k] | ((k + 1 < 2 + N ? h[k + 1] : 0u) << 16);
+              q[1] = make_uint4(r[0], r[1], r[2], r[3]);
+            }
             continue;
           }
         }
@@ -1369,11 +1387,24 @@ template <int N, int DROP, int ERASE>
 __global__ void __launch_bounds__(256) k_merge_fixup(const __grid_constant__ MergeArgs a) {
   constexpr bool kErase = (ERASE != 0) && (N >= 2);
   constexpr float kKS = ERASE == 2 ? 1.f : 0x1p24f;  // the fast kernel's scaled domain (sr32 for fast_opp_bits)
+  // blockIdx.y splits one CTA's queue over several blocks: every element is a chain of dependent
+  // global loads (segment -> pointers -> data), so the kernel needs many threads in flight
   const uint32_t n = a.fix_count[blockIdx.x];
-  for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
-    const uint2 e = a.fix_q[(uint64_t)blockIdx.x * a.fix_cap + k];
-    const rlk_fusion_segment* seg = a.plan.segs + e.x;
-    const uint64_t idx = e.y;
+  for (uint32_t k = blockIdx.y * blockDim.x + threadIdx.x; k < n; k += blockDim.x * gridDim.y) {
+    const uint4* q = a.fix_q + ((uint64_t)blockIdx.x * a.fix_cap + k) * kFixWords<N>;
+    uint32_t h[2 * 4 * kFixWords<N>];  // the entry as u32 words
+    {
+      const uint4 q0 = q[0];
+      h[0] = q0.x; h[1] = q0.y; h[2] = q0.z; h[3] = q0.w;
+      if constexpr (kFixWords<N> > 1) {
+        const uint4 q1 = q[1];
+        h[4] = q1.x; h[5] = q1.y; h[6] = q1.z; h[7] = q1.w;
+      }
+    }
+    auto half = [&](int m) { return (h[2 + m / 2] >> (16 * (m & 1))) & 0xffffu; };  // bf16 input m (0 = base)
+    const rlk_fusion_segment* seg = a.plan.segs + (h[0] & 0xffffffu);
+    const uint32_t keep = h[0] >> 24;
+    const uint64_t idx = h[1];
     const uint32_t t = seg->tensor;
     ElemConsts c;
     float sr32[N];
@@ -1382,18 +1413,14 @@ __global__ void __launch_bounds__(256) k_merge_fixup(const __grid_constant__ Mer
       c.scale[i] = a.scale[(uint64_t)t * N + i];
       sr32[i] = (float)(DROP ? c.scale[i] / a.keep_prob : c.scale[i]) * kKS;
     }
-    const uint16_t bb = reinterpret_cast<const uint16_t*>(seg->base)[idx];
     float xf[N];
     double X[N];
-    uint32_t keep = 0;
-    const uint64_t j = seg->j0 + idx;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      xf[i] = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(seg->expert[i])[idx] << 16);
+      xf[i] = __uint_as_float(half(1 + i) << 16);
       X[i] = (double)xf[i];
-      keep |= (DROP ? ((a.bitmap[(uint64_t)i * a.words_per_row + (j >> 5)] >> (j & 31)) & 1u) : 1u) << i;
     }
-    const float bf = __uint_as_float((uint32_t)bb << 16);
+    const float bf = __uint_as_float(half(0) << 16);
     uint32_t nzm, erm;
     const double Y = merge_elem_f64<N>((double)bf, X, keep, a, c, nzm, erm);
     reinterpret_cast<uint16_t*>(seg->out)[idx] = f64_to_bf16_rne(Y);
@@ -1470,13 +1497,13 @@ static int launch_merge_fast(MergeArgs& a, cudaStream_t s) {
   a.sub_shift = sub_shift_for(a.plan.n_items, cap, kItem / kFastSB * 2);
   uint32_t grid = std::min<uint32_t>(a.plan.n_items << a.sub_shift, cap);
   if (a.fix_q) {
-    a.fix_cap = (uint32_t)std::min<uint64_t>(a.fix_cap_total / grid, 0xffffffffu);
-    if (a.fix_cap == 0) a.fix_q = nullptr;
+    a.fix_cap = (uint32_t)std::min<uint64_t>(a.fix_cap_total / kFixWords<N> / grid, 0xffffffffu);
+    if (a.fix_cap == 0 || a.plan.n_segs >= (1u << 24)) a.fix_q = nullptr;
   }
   kern<<<grid, kFastThreads, smem, s>>>(a);
   if (int st = launch_status("rlk_fusion_merge")) return st;
   if (a.fix_q) {
-    k_merge_fixup<N, DROP, ERASE><<<grid, 256, 0, s>>>(a);
+    k_merge_fixup<N, DROP, ERASE><<<dim3(grid, 8), 256, 0, s>>>(a);
     return launch_status("rlk_fusion_merge (fix-up)");
   }
   return RLK_OK;
@@ -1687,8 +1714,8 @@ int rlk_fusion_merge_ws(const rlk_fusion_plan* plan, int n_experts, int dtype_in
   // workspace: [per-CTA queue lengths: 4 KiB | queue entries (8 B each)]
   if (workspace && workspace_bytes > RLK_MERGE_WS_HEADER && ((uintptr_t)workspace & 15u) == 0) {
     a.fix_count = (uint32_t*)workspace;
-    a.fix_q = (uint2*)((char*)workspace + RLK_MERGE_WS_HEADER);
-    a.fix_cap_total = (workspace_bytes - RLK_MERGE_WS_HEADER) / sizeof(uint2);
+    a.fix_q = (uint4*)((char*)workspace + RLK_MERGE_WS_HEADER);
+    a.fix_cap_total = (workspace_bytes - RLK_MERGE_WS_HEADER) / sizeof(uint4);  // in uint4 words
   }
   cudaStream_t s = (cudaStream_t)stream;
   switch (dtype_in) {
