@@ -1272,8 +1272,50 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
 #ifdef RLK_TIMING_SKIP_PHASE2  // diagnostic builds only (tools/build_variant.py): phase 2 not run
       slowbits = 0;
 #endif
-      // phase 2 (rare): exact reference-order evaluation of the recorded elements, read back from the
-      // stage; the 2-byte store follows this thread's own vector store of the same word
+      // phase 2a: the flagged elements go to the fix-up queue -- one shared-memory atomic per warp
+      // (warp prefix sum of the lanes' counts), then each lane writes its entries
+      if (a.fix_q && __any_sync(0xffffffffu, slowbits != 0u)) {
+        const uint32_t c = __popc(slowbits);
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t base = 0;
+        if (lane == 31) base = atomicAdd(&fix_n, tot);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        if (base + tot <= a.fix_cap) {
+          uint32_t slot = base + incl - c;
+          while (slowbits) {
+            const uint32_t bpos = __ffs(slowbits) - 1;
+            slowbits &= slowbits - 1;
+            const uint32_t le = (tid + (bpos / kFastElems) * kFastCThreads) * kFastElems + (bpos % kFastElems);
+            uint32_t h[2 + N], keep = 0;
+            h[0] = reinterpret_cast<const uint16_t*>(sb)[le];
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              h[1 + i] = reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le];
+              keep |= DROP ? (((uint32_t)bm[i * BMB + (le >> 3)] >> (le & 7)) & 1u) << i : (1u << i);
+            }
+            h[1 + N] = 0;
+            uint4* qe = a.fix_q + ((uint64_t)blockIdx.x * a.fix_cap + slot++) * kFixWords<N>;
+            qe[0] = make_uint4(cur.lo | (keep << 24), (uint32_t)(out_base + le), h[0] | (h[1] << 16),
+                               N >= 2 ? (h[2] | (h[3] << 16)) : 0u);
+            if constexpr (kFixWords<N> > 1) {
+              uint32_t r[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int k = 4; k < 2 + N; k += 2) r[(k - 4) / 2] = h[k] | ((k + 1 < 2 + N ? h[k + 1] : 0u) << 16);
+              qe[1] = make_uint4(r[0], r[1], r[2], r[3]);
+            }
+          }
+        } else if (lane == 31) {
+          atomicSub(&fix_n, tot);  // the queue is full: this warp finishes its elements below
+        }
+      }
+      // phase 2b (queue full, or no queue): exact reference-order evaluation of the recorded elements,
+      // read back from the stage; the 2-byte store follows this thread's own vector store of the word
       while (slowbits) {
         const uint32_t bpos = __ffs(slowbits) - 1;
         slowbits &= slowbits - 1;
@@ -1288,7 +1330,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
           keep |= DROP ? (((uint32_t)bm[i * BMB + (le >> 3)] >> (le & 7)) & 1u) << i : (1u << i);
         }
         if constexpr (ERASE == 1) {
-          if (tie_ok) {  // exact sum-vote ties certified in scalar f32 (the common flag without normalisation)
+          if (tie_ok) {  // exact sum-vote ties certified in scalar f32
             uint32_t xb[N], fo = 0;
             uint16_t wout;
 #pragma unroll
@@ -1303,29 +1345,6 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) k_merge_fast(const __
               outp[out_base + le] = wout;
               continue;
             }
-          }
-        }
-        if (a.fix_q) {
-          // defer to k_merge_fixup: one warp lane here would hold 31 idle lanes for the whole f64
-          // evaluation; the fix-up kernel runs the queued elements one per thread.  The entry carries
-          // the keep bits and the bf16 inputs (from the stage), so the fix-up reads no parameters.
-          const uint32_t slot = atomicAdd(&fix_n, 1u);
-          if (slot < a.fix_cap) {
-            uint32_t h[2 + N];
-            h[0] = reinterpret_cast<const uint16_t*>(sb)[le];
-#pragma unroll
-            for (int i = 0; i < N; ++i) h[1 + i] = reinterpret_cast<const uint16_t*>(sb + (i + 1) * SB)[le];
-            h[1 + N] = 0;
-            uint4* q = a.fix_q + ((uint64_t)blockIdx.x * a.fix_cap + slot) * kFixWords<N>;
-            q[0] = make_uint4(cur.lo | (keep << 24), (uint32_t)(out_base + le), h[0] | (h[1] << 16),
-                              N >= 2 ? (h[2] | (h[3] << 16)) : 0u);
-            if constexpr (kFixWords<N> > 1) {
-              uint32_t r[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-              for (int k = 4; k < 2 + N; k += 2) r[(k - 4) / 2] = h[k] | ((k + 1 < 2 + N ? h[k + 1] : 0u) << 16);
-              q[1] = make_uint4(r[0], r[1], r[2], r[3]);
-            }
-            continue;
           }
         }
         uint32_t nzm, erm;
@@ -1390,6 +1409,11 @@ __global__ void __launch_bounds__(256) k_merge_fixup(const __grid_constant__ Mer
   // blockIdx.y splits one CTA's queue over several blocks: every element is a chain of dependent
   // global loads (segment -> pointers -> data), so the kernel needs many threads in flight
   const uint32_t n = a.fix_count[blockIdx.x];
+  uint32_t c_seg = 0xffffffffu;  // per-segment constants, reloaded only when the segment changes
+  const rlk_fusion_segment* seg = nullptr;
+  uint32_t t = 0;
+  ElemConsts c;
+  float sr32[N];
   for (uint32_t k = blockIdx.y * blockDim.x + threadIdx.x; k < n; k += blockDim.x * gridDim.y) {
     const uint4* q = a.fix_q + ((uint64_t)blockIdx.x * a.fix_cap + k) * kFixWords<N>;
     uint32_t h[2 * 4 * kFixWords<N>];  // the entry as u32 words
@@ -1402,16 +1426,17 @@ __global__ void __launch_bounds__(256) k_merge_fixup(const __grid_constant__ Mer
       }
     }
     auto half = [&](int m) { return (h[2 + m / 2] >> (16 * (m & 1))) & 0xffffu; };  // bf16 input m (0 = base)
-    const rlk_fusion_segment* seg = a.plan.segs + (h[0] & 0xffffffu);
     const uint32_t keep = h[0] >> 24;
     const uint64_t idx = h[1];
-    const uint32_t t = seg->tensor;
-    ElemConsts c;
-    float sr32[N];
+    if ((h[0] & 0xffffffu) != c_seg) {
+      c_seg = h[0] & 0xffffffu;
+      seg = a.plan.segs + c_seg;
+      t = seg->tensor;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      c.scale[i] = a.scale[(uint64_t)t * N + i];
-      sr32[i] = (float)(DROP ? c.scale[i] / a.keep_prob : c.scale[i]) * kKS;
+      for (int i = 0; i < N; ++i) {
+        c.scale[i] = a.scale[(uint64_t)t * N + i];
+        sr32[i] = (float)(DROP ? c.scale[i] / a.keep_prob : c.scale[i]) * kKS;
+      }
     }
     float xf[N];
     double X[N];

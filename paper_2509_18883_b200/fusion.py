@@ -457,20 +457,21 @@ class FusionCall:
                          L.ptr(ws), ws.numel(), s)
         return self
 
-    # fix-up queue of the bf16 fast merge.  With normalisation a step flags ~1 element in 1,500 (their
-    # f32 bracket straddles a bf16 rounding boundary): the queue holds 1/1024 of the local elements and
-    # the fix-up kernel finishes them in ~0.1 ms instead of ~0.6 ms of warp-serial work in the merge.
-    # Without normalisation (target_norm=None) the arithmetic is exact enough that ~2% of the results
-    # land exactly on bf16 midpoints (b + (2/3) m u crossing a binade): re-reading their inputs from
-    # global memory costs as much as finishing them in the merge, so there is no queue.  Overflow falls
-    # back to the in-kernel exact path (same results).
+    # fix-up queue of the bf16 fast merge (16 bytes per entry for up to 3 experts, 32 beyond).  With
+    # normalisation a step flags ~1 element in 2,300 (their f32 bracket straddles a bf16 rounding
+    # boundary): room for 1/1024 of the local elements.  Without it (target_norm=None) the arithmetic is
+    # exact enough that ~2% of the results land exactly on bf16 midpoints (b + (2/3) m u crossing a
+    # binade): room for 1/16.  Overflow falls back to the in-kernel exact path (same results, slower).
     def _merge_workspace(self) -> torch.Tensor:
-        if not self.fixup or self.cfg.target_norm is None:
+        if not self.fixup:
             return torch.empty(0, dtype=torch.uint8, device=self.device)
         ws = getattr(self, "_ws", None)
         if ws is None:
-            entries = min(max(self.plan.local_elems // 1024, 1 << 17), 64 << 20)
-            ws = torch.empty(L.RLK_MERGE_WS_HEADER + 8 * entries, dtype=torch.uint8, device=self.device)
+            frac = 16 if self.cfg.target_norm is None else 1024
+            per = 16 if self.n <= 3 else 32
+            entries = min(max(self.plan.local_elems // frac, 1 << 16), (8 << 30) // per)
+            ws = torch.empty(L.RLK_MERGE_WS_HEADER + per * entries, dtype=torch.uint8, device=self.device)
+            ws[:L.RLK_MERGE_WS_HEADER].zero_()  # queue lengths of CTAs a launch does not use read as 0
             self._ws = ws
         return ws
 
