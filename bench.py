@@ -33,6 +33,10 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "fusion params/s & HBM GB/s (%roofline) at 1/2/4/8 B200; GRPO loss tokens/s"
 N_EXPERTS = 3
+# K3 is launched through rlk_fusion_merge_ws (merge + fix-up queue); its per-call CUDA-event time
+# includes the fix-up kernel.  profiles/traffic.json keys the ncu traffic by the kernel family.
+MERGE_CALL = "rlk_fusion_merge_ws"
+TRAFFIC_KEY = {MERGE_CALL: "rlk_fusion_merge"}
 
 
 def measured_peak_gbs() -> tuple[float, str]:
@@ -837,7 +841,7 @@ def main():
             sub = argparse.Namespace(**{**vars(args), "layout": lay, "dtype": dt, "quick": True, "no_e2e": True})
             r = fusion_bench(sub, rank, world, local, group)
             es_ = {"bf16": 2, "f32": 4}[dt]
-            kb_ = {"rlk_fusion_sumsq": (N_EXPERTS + 1) * es_, "rlk_fusion_merge": (N_EXPERTS + 1) * es_ + es_}
+            kb_ = {"rlk_fusion_sumsq": (N_EXPERTS + 1) * es_, MERGE_CALL: (N_EXPERTS + 1) * es_ + es_}
             kern_ = {k: v for k, v in r["kern_local"].items() if k in kb_}
             dom_ = max(kern_, key=kern_.get)
             ach_ = r["local_params"] * kb_[dom_] / (kern_[dom_] / 1e3) / 1e9
@@ -868,7 +872,7 @@ def main():
     value = total / (ms / 1e3)
     # dominant kernel roofline (rank 0's launches; algorithmic bytes = SURVEY 8(d) per-param figures)
     es = {"bf16": 2, "f32": 4}[args.dtype]
-    kb = {"rlk_fusion_sumsq": (N_EXPERTS + 1) * es, "rlk_fusion_merge": (N_EXPERTS + 1) * es + es}
+    kb = {"rlk_fusion_sumsq": (N_EXPERTS + 1) * es, MERGE_CALL: (N_EXPERTS + 1) * es + es}
     kern = {k: v for k, v in fz["kern_local"].items() if k in kb}
     dom = max(kern, key=kern.get)
     achieved = fz["local_params"] * kb[dom] / (kern[dom] / 1e3) / 1e9
@@ -877,7 +881,7 @@ def main():
     if tfile.exists():
         try:
             tj = json.loads(tfile.read_text())
-            traffic = tj.get(args.layout, {}).get(f"{world}", {}).get(dom)
+            traffic = tj.get(args.layout, {}).get(f"{world}", {}).get(TRAFFIC_KEY.get(dom, dom))
         except Exception:
             traffic = None
     step_gbs = (total * es * (N_EXPERTS + 1) * 2 + total * es) / (ms / 1e3) / 1e9

@@ -80,7 +80,7 @@ for rep, out in (("fusion_full", "ncu_fusion_summary"), ("grpo_full", "ncu_grpo_
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             b = float(rd.replace(",", "")) * mult.get(u["dram__bytes_read.sum"], 1) + \
                 float(wr.replace(",", "")) * mult.get(u["dram__bytes_write.sum"], 1)
-            key = "rlk_fusion_merge" if "k_merge" in name else "rlk_fusion_sumsq" if "k_sumsq" in name else \
+            key = "rlk_fusion_merge_fixup" if "k_merge_fixup" in name else "rlk_fusion_merge" if "k_merge" in name else "rlk_fusion_sumsq" if "k_sumsq" in name else \
                 "rlk_fusion_mask_bitmap" if "k_mask" in name else name.split("(")[0]
             traffic.setdefault(key, []).append(b)
             txt.append(f"    {'dram bytes read + write':60s} {b:18.0f} byte")
