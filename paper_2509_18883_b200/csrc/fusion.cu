@@ -248,8 +248,12 @@ struct SumsqArgs {
 };
 
 // Two CTAs per SM: the loop is bound by F2F (XU pipe) and fp64 latency, so it needs the warps.
-template <int DT, int N>
+// CM >= 0 (f32 pair mode): the counting mode fixed at compile time -- 0 no counters, 1 every entry
+// kept, 2 keep bits from the K2 bitmap -- and the non-zero test done on the f32 inputs (x != b; the
+// inputs are finite whenever the counts are used: non-finite norms fail the call).
+template <int DT, int N, int CM = -1>
 __global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ SumsqArgs a) {
+  static_assert(CM < 0 || DT == RLK_F32, "compile-time counting mode: f32 pair mode only");
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DT>::size;
   constexpr int VEC = 16 / ESZ;
@@ -257,8 +261,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ S
   constexpr uint32_t ELEMS = SB / ESZ;
   constexpr uint32_t BMB = ELEMS / 8;
   const Ring r = ring_setup(smem, a.stage_bytes, a.nstages);
-  const bool delta = a.delta_mode != 0;
-  const bool count = a.counters != nullptr;
+  const bool delta = CM >= 0 ? false : a.delta_mode != 0;
+  const bool count = CM >= 0 ? CM != 0 : a.counters != nullptr;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kCWarps) {
     if (lane == 0) produce<ESZ, N, StreamBytes<N>::v, false>(a.plan, r, !delta, (count && a.dropout_mode == 2) ? a.bitmap : nullptr,
@@ -289,6 +293,31 @@ __global__ void __launch_bounds__(kThreads, 2) k_sumsq(const __grid_constant__ S
       const uint32_t nvec = main_elems / VEC;
       for (uint32_t v = tid; v < nvec; v += kCThreads) {
         const uint32_t le = v * VEC;
+        if constexpr (CM >= 0) {
+          const uint4 bq = lds128(sb + v * 16);
+          double b[4];
+          VecIO<RLK_F32>::f64(bq, b);
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            const uint4 xq = lds128(sb + (i + 1) * SB + v * 16);
+            double x[4];
+            VecIO<RLK_F32>::f64(xq, x);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const double d = x[e] - b[e];
+              acc[i][e & 1] = fma(d, d, acc[i][e & 1]);
+            }
+            if constexpr (CM != 0) {
+              const uint32_t neq = (uint32_t)(__uint_as_float(xq.x) != __uint_as_float(bq.x)) |
+                                   (uint32_t)(__uint_as_float(xq.y) != __uint_as_float(bq.y)) << 1 |
+                                   (uint32_t)(__uint_as_float(xq.z) != __uint_as_float(bq.z)) << 2 |
+                                   (uint32_t)(__uint_as_float(xq.w) != __uint_as_float(bq.w)) << 3;
+              const uint32_t keep = CM == 2 ? (uint32_t)(bm[i * BMB + (le >> 3)] >> (le & 7)) : 0xfu;
+              nz[i] += __popc(neq & keep & 0xfu);
+            }
+          }
+          continue;
+        }
         double b[VEC];
         if (!delta) VecIO<DT>::f64(lds128(sb + v * 16), b);
         else {
@@ -638,6 +667,94 @@ __device__ __forceinline__ double merge_elem_f64(double B, const double* X, uint
   return Y;
 }
 
+// The same reference-order f64 evaluation with the dropout / erase modes fixed at compile time (DROP 0
+// none, 2 bitmap; ERASE 0 off, 1 sum, 2 squared) for base + experts in pair mode.  s[i] is the
+// normalisation scale, or with FOLD the scale times 1/keep_prob: when 1/keep_prob is a power of two
+// and s[i] >= 2^-873, RN(RN(d s) / keep_prob) == RN(d (s / keep_prob)) for every difference d of two
+// f32 values (|d| >= 2^-149 when non-zero, so d s never underflows), saving the Markstein division.
+template <int N, int DROP, int ERASE, bool FOLD>
+__device__ __forceinline__ double merge_elem_spec(double B, const double* X, uint32_t keep, const MergeArgs& a,
+                                                  const double* s, uint32_t& er) {
+  double K[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double k = __dmul_rn(__dsub_rn(X[i], B), s[i]);
+    if constexpr (DROP != 0) {
+      if constexpr (!FOLD) k = div_rn(k, a.keep_prob, a.inv_keep);
+      k = ((keep >> i) & 1u) ? k : 0.0;
+    }
+    K[i] = k;
+  }
+  er = 0;
+  if constexpr (N >= 2 && ERASE != 0) {
+    double V;
+    if constexpr (ERASE == 1) {
+      V = K[0];
+#pragma unroll
+      for (int i = 1; i < N; ++i) V = __dadd_rn(V, K[i]);
+    } else {
+      auto sq = [](double k) {
+        const double m = __dmul_rn(k, k);
+        return k > 0.0 ? m : (k < 0.0 ? -m : __dmul_rn(k, m));  // sign(k) * k^2 (sign(0) = 0, NaN stays NaN)
+      };
+      V = sq(K[0]);
+#pragma unroll
+      for (int i = 1; i < N; ++i) V = __dadd_rn(V, sq(K[i]));
+    }
+    const bool vp = V > 0.0, vn = V < 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if ((vp && K[i] < 0.0) || (vn && K[i] > 0.0)) {
+        K[i] = 0.0;
+        er |= 1u << i;
+      }
+    }
+  }
+  double Y = B;
+#pragma unroll
+  for (int i = 0; i < N; ++i) Y = __dadd_rn(Y, __dmul_rn(a.w[i], K[i]));
+  return Y;
+}
+
+// One ring stage of the specialised f32 merge: VEC = 4 elements per 16-byte vector, the keep bits of a
+// vector read as one 4-bit field per expert.
+template <int N, int DROP, int ERASE, bool FOLD>
+__device__ __forceinline__ void merge_stage_f32(const uint8_t* sb, const uint8_t* bm, uint32_t nvec, int tid,
+                                                const MergeArgs& a, const double* s, void* out, uint64_t out_base,
+                                                uint32_t* cnt_er) {
+  constexpr uint32_t SB = StreamBytes<N>::v;
+  constexpr uint32_t BMW = SB / 4 / 32;  // bitmap words per expert per stage
+  for (uint32_t v = tid; v < nvec; v += kCThreads) {
+    const uint32_t le = v * 4;
+    double b[4], x[N][4];
+    VecIO<RLK_F32>::f64(lds128(sb + v * 16), b);
+#pragma unroll
+    for (int i = 0; i < N; ++i) VecIO<RLK_F32>::f64(lds128(sb + (i + 1) * SB + v * 16), x[i]);
+    uint32_t kb[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      kb[i] = 0xfu;
+      if constexpr (DROP != 0) kb[i] = reinterpret_cast<const uint32_t*>(bm)[i * BMW + (le >> 5)] >> (le & 31);
+    }
+    double y[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      double X[N];
+      uint32_t keep = 0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        X[i] = x[i][e];
+        keep |= ((kb[i] >> e) & 1u) << i;
+      }
+      uint32_t erm;
+      y[e] = merge_elem_spec<N, DROP, ERASE, FOLD>(b[e], X, keep, a, s, erm);
+#pragma unroll
+      for (int i = 0; i < N; ++i) cnt_er[i] += (erm >> i) & 1u;
+    }
+    store_vec_f64<RLK_F32, 4>(out, out_base + le, y);
+  }
+}
+
 template <int N, int VEC>
 __device__ __forceinline__ uint32_t keep_bits_for(const MergeArgs& a, const uint8_t* bm_stage, uint32_t bm_stride,
                                                   uint32_t local_elem, uint64_t jglobal, int e) {
@@ -785,8 +902,12 @@ __device__ __forceinline__ uint32_t word_of(const uint4& q, int p) {
 }
 
 // Generic K3: the reference-order f64 path for every dtype combination (and the tails).
-template <int DTI, int DTO, int N>
+// SPEC != 0 (f32 -> f32 pair mode, 2..4 experts): the modes are compile-time, SPEC = 1 + 3 * (DROP / 2) + ERASE.
+template <int DTI, int DTO, int N, int SPEC = 0>
 __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid_constant__ MergeArgs a) {
+  static_assert(SPEC == 0 || (DTI == RLK_F32 && DTO == RLK_F32 && N >= 2 && N <= 4), "specialised merge: f32 only");
+  constexpr int SDROP = SPEC ? 2 * ((SPEC - 1) / 3) : 0;
+  constexpr int SERASE = SPEC ? (SPEC - 1) % 3 : 0;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int ESZ = Elem<DTI>::size;
   constexpr int VEC = 16 / ESZ;
@@ -816,6 +937,20 @@ __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid
     ElemConsts c;
 #pragma unroll
     for (int i = 0; i < N; ++i) c.scale[i] = __ldg(scale + i);
+    // specialised path: fold 1/keep_prob into the scale when that is exact (see merge_elem_spec)
+    bool fold = false;
+    double sf[N];
+    if constexpr (SPEC != 0) {
+      fold = SDROP != 0 && (__double_as_longlong(a.inv_keep) & 0x000fffffffffffffull) == 0 &&
+             __dmul_rn(a.inv_keep, a.keep_prob) == 1.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        sf[i] = __dmul_rn(c.scale[i], a.inv_keep);
+        fold = fold && (c.scale[i] == 0.0 || c.scale[i] >= 0x1p-873) && fabs(sf[i]) < INFINITY;
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) sf[i] = fold ? sf[i] : c.scale[i];
+    }
     uint32_t cnt_er[N];  // entries erased (non-zero entries after dropout are counted by K1)
 #pragma unroll
     for (int i = 0; i < N; ++i) cnt_er[i] = 0;
@@ -829,7 +964,10 @@ __global__ void __launch_bounds__(kThreads, N <= 5 ? 2 : 1) k_merge(const __grid
       const uint8_t* bm = sb + (N + 1) * SB;
       const uint32_t nvec = main_elems / VEC;
       const uint64_t out_base = g.start + off;
-      {
+      if constexpr (SPEC != 0) {
+        if (fold) merge_stage_f32<N, SDROP, SERASE, true>(sb, bm, nvec, tid, a, sf, g.out, out_base, cnt_er);
+        else merge_stage_f32<N, SDROP, SERASE, false>(sb, bm, nvec, tid, a, sf, g.out, out_base, cnt_er);
+      } else {
         // ---------------- reference-order f64 path
         for (uint32_t v = tid; v < nvec; v += kCThreads) {
           const uint32_t le = v * VEC;
@@ -1464,9 +1602,12 @@ __global__ void __launch_bounds__(256) k_merge_fixup(const __grid_constant__ Mer
 // K3 work-unit split for layouts with fewer items than ~2 waves of CTAs (config 1: 154 items on 296
 // CTA slots): 2^s units per item, at most one ring stage per unit apart (`stages_per_item`), so every
 // CTA slot gets work.  Large layouts keep whole items (s = 0).
+// Work units of 65536 >> s elements for layouts with few items: split until there are >= 8 units per
+// CTA (the CTAs stride over units, so the last round is at most 1/8 of the work: config 1's 153 items
+// over 296 CTAs were 2 or 3 whole-item halves per CTA, 27% idle), keeping >= 2 ring stages per unit.
 static uint32_t sub_shift_for(uint32_t n_items, uint32_t cap, uint32_t stages_per_item) {
   uint32_t s = 0;
-  while (s < 3 && (n_items << s) < 2 * cap && (1u << (s + 1)) <= stages_per_item) ++s;
+  while (s < 5 && (uint64_t(n_items) << s) < 8ull * cap && (1u << (s + 1)) <= stages_per_item) ++s;
   return s;
 }
 
@@ -1495,6 +1636,10 @@ static int launch_sumsq(SumsqArgs& a, cudaStream_t s) {
   a.nstages = ns;
   const uint32_t smem = 1024 + sb * ns;
   auto kern = k_sumsq<DT, N>;
+  if constexpr (DT == RLK_F32) {
+    if (!a.delta_mode && !(a.counters && a.dropout_mode == 1))
+      kern = !a.counters ? k_sumsq<DT, N, 0> : (a.dropout_mode == 2 ? k_sumsq<DT, N, 2> : k_sumsq<DT, N, 1>);
+  }
   if constexpr (DT == RLK_BF16 && N <= 4) {
     // pair mode with no inline dropout draws: the bf16 fast kernel
     if (!a.delta_mode && !(a.counters && a.dropout_mode == 1)) {
@@ -1564,6 +1709,14 @@ static int launch_merge(MergeArgs& a, cudaStream_t s) {
   if (ctas == 2) a.nstages = ns = std::max<uint32_t>(2u, std::min<uint32_t>(ns / 2, 4u));
   const uint32_t smem = 1024 + sb * ns;
   auto kern = k_merge<DTI, DTO, N>;
+  if constexpr (DTI == RLK_F32 && DTO == RLK_F32 && N >= 2 && N <= 4) {
+    // f32 checkpoints: the compile-time-mode kernel (same arithmetic; exact_path keeps the generic one)
+    if (a.fast && !a.delta_mode && a.with_base && a.dropout_mode != 1 && a.erase_mode >= 0 && a.erase_mode <= 2) {
+      const int d = a.dropout_mode == 2 ? 1 : 0, e = a.erase_mode;
+      kern = d ? (e == 0 ? k_merge<DTI, DTO, N, 4> : e == 1 ? k_merge<DTI, DTO, N, 5> : k_merge<DTI, DTO, N, 6>)
+               : (e == 0 ? k_merge<DTI, DTO, N, 1> : e == 1 ? k_merge<DTI, DTO, N, 2> : k_merge<DTI, DTO, N, 3>);
+    }
+  }
   int st = ensure_smem(kern, smem);
   if (st) return st;
   const uint32_t cap = ctas * (uint32_t)sm_count();

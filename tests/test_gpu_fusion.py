@@ -417,3 +417,43 @@ def test_fast_path_overflow_falls_back(cuda):
         ref, _ = OF.fuse(base, experts, **cfgkw)
         got = outs[0].view(torch.int16).cpu().numpy().view(np.uint16)
         assert int((got != rne_bf16_bits(ref)).sum()) == 0, cfgkw
+
+
+F32_CASES = [
+    (2, dict()), (4, dict()), (2, dict(dropout_p=0.5, seed=1)), (4, dict(dropout_p=0.75, seed=9)),
+    (3, dict(dropout_p=0.75, seed=5, erase_weighting="squared")), (4, dict(dropout_p=0.2, seed=3, erase_mode=False)),
+    (2, dict(dropout_p=0.5, seed=8, target_norm=None, erase_mode=False)),
+    (4, dict(dropout_p=0.5, seed=2, target_norm=2.0, merge_weights=(0.4, 0.3, 0.2, 0.1))),
+    (3, dict(dropout_p=0.6, seed=4, erase_weighting="squared", merge_weights=(0.5, 0.375, 0.125))),
+]
+
+
+@pytest.mark.parametrize("n,cfgkw", F32_CASES)
+def test_f32_specialised_merge_vs_oracle(cuda, n, cfgkw):
+    """f32 checkpoints run the compile-time-mode K3 (k_merge<f32, f32, N, SPEC>; with keep_prob a power of
+    two the dropout rescale is folded into the scale): bit-identical to the reference-order f64 result
+    rounded to f32, and to the generic kernel (exact_merge), for 2-4 experts and every mode."""
+    from paper_2509_18883_b200 import fusion as F
+    rnd = lambda x: np.asarray(x, np.float32).astype(np.float64)
+    base, experts = synth_state_dicts(mlp_dict_shapes(8), n, seed=11 + n, dtype_round=rnd)
+    # adversarial columns: exact zero deltas, vote ties, a huge and a subnormal-scale delta
+    for name in base:
+        b = base[name].reshape(-1)
+        for i, e in enumerate(experts):
+            v = e[name].reshape(-1)
+            v[:64] = b[:64]
+            v[64:96] = rnd(b[64:96] + (1e-3 if i % 2 == 0 else -1e-3))
+            v[96] = rnd(b[96] + 3e4 * (i + 1))
+            v[97] = rnd(b[97] + 1e-40)
+    to = lambda d: {k: torch.from_numpy(v).to(cuda, torch.float32) for k, v in d.items()}
+    cfg = F.FusionConfig(**cfgkw)
+    outs, rep = F.fuse_state_dict(to(base), [to(e) for e in experts], cfg)
+    outs_x, rep_x = F.fuse_state_dict(to(base), [to(e) for e in experts], cfg, exact_merge=True)
+    ref, rstats = _oracle_dict(base, experts, cfgkw)
+    for name in base:
+        got = outs[name].reshape(-1).cpu().numpy()
+        np.testing.assert_array_equal(got, ref[name].astype(np.float32), err_msg=name)
+        np.testing.assert_array_equal(got.view(np.uint32), outs_x[name].reshape(-1).cpu().numpy().view(np.uint32))
+        st = rep.stats(name)
+        assert list(st.erased_counts) == rstats[name]["erased"] == list(rep_x.stats(name).erased_counts), name
+        assert list(st.dropout_kept_fraction) == rstats[name]["kept"], name

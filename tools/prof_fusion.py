@@ -14,6 +14,7 @@ ap.add_argument("--layout", default="gpt1p3b")
 ap.add_argument("--dropout", type=float, default=0.5)
 ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--grpo", action="store_true")
+ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 if a.grpo:
@@ -33,10 +34,11 @@ if a.grpo:
     sys.exit(0)
 shapes = LAYOUTS[a.layout]()
 base, experts = {}, [dict() for _ in range(3)]
+dt = {"bf16": torch.bfloat16, "f32": torch.float32}[a.dtype]
 for t, (k, s) in enumerate(shapes.items()):
-    base[k] = torch.empty(s, dtype=torch.bfloat16, device=dev)
+    base[k] = torch.empty(s, dtype=dt, device=dev)
     for e in experts:
-        e[k] = torch.empty(s, dtype=torch.bfloat16, device=dev)
+        e[k] = torch.empty(s, dtype=dt, device=dev)
     fill_synthetic(base[k].view(-1), [e[k].view(-1) for e in experts], t)
 cfg = F.FusionConfig(dropout_p=a.dropout, seed=42)
 for _ in range(a.runs):
