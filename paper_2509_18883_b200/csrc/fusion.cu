@@ -704,10 +704,9 @@ __device__ __forceinline__ double merge_elem_spec(double B, const double* X, uin
     const bool vp = V > 0.0, vn = V < 0.0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      if ((vp && K[i] < 0.0) || (vn && K[i] > 0.0)) {
-        K[i] = 0.0;
-        er |= 1u << i;
-      }
+      const bool opp = (vp & (K[i] < 0.0)) | (vn & (K[i] > 0.0));  // no short-circuit branches
+      K[i] = opp ? 0.0 : K[i];
+      er |= (uint32_t)opp << i;
     }
   }
   double Y = B;
