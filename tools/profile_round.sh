@@ -16,4 +16,8 @@ ncu --set full --clock-control none --import-source on -k "regex:k_merge_fast|k_
 python tools/prof_grpo_fused.py > $OUT/prof_grpo_plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k "regex:k_grpo" -s 4 -c 4 -o $OUT/grpo_full python tools/prof_grpo_fused.py > $OUT/ncu_grpo.log 2>&1
 python bench.py --stream --stream-layers 1 --steps 3 --warmup 3 --json-out $OUT/config4_stream.json > $OUT/config4_stream.log 2>&1
+python tools/prof_fusion.py --layout mlp10m --dtype f32 --runs 3 > $OUT/prof_c1_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k "regex:k_merge|k_sumsq" -s 2 -c 2 -o $OUT/config1_full python tools/prof_fusion.py --layout mlp10m --dtype f32 --runs 3 > $OUT/ncu_config1.log 2>&1
+python tools/step_gap.py > $OUT/step_gap.log 2>&1
+python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1
 ls -la $OUT

@@ -29,6 +29,10 @@ if (src / "bench_reference.log").exists():
     if ref:
         (dst / f"{tag}_bench_reference.json").write_text(json.dumps(json.loads(ref[-1]), indent=1))
 
+for extra in ("pytest_gpu.log", "step_gap.log"):
+    if (src / extra).exists():
+        shutil.copy(src / extra, dst / f"{tag}_{extra}")
+
 # 2. launch list -> per-kernel averages and the fusion-step shares
 rows = list(csv.reader(open(src / "launches.csv")))
 hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -59,7 +63,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic"]
 traffic = {}
-for rep, out in (("fusion_full", "ncu_fusion_summary"), ("grpo_full", "ncu_grpo_summary")):
+for rep, out in (("fusion_full", "ncu_fusion_summary"), ("grpo_full", "ncu_grpo_summary"),
+                 ("config1_full", "ncu_config1_summary")):
     f = src / f"{rep}.ncu-rep"
     if not f.exists():
         continue
@@ -82,7 +87,8 @@ for rep, out in (("fusion_full", "ncu_fusion_summary"), ("grpo_full", "ncu_grpo_
                 float(wr.replace(",", "")) * mult.get(u["dram__bytes_write.sum"], 1)
             key = "rlk_fusion_merge_fixup" if "k_merge_fixup" in name else "rlk_fusion_merge" if "k_merge" in name else "rlk_fusion_sumsq" if "k_sumsq" in name else \
                 "rlk_fusion_mask_bitmap" if "k_mask" in name else name.split("(")[0]
-            traffic.setdefault(key, []).append(b)
+            if rep == "fusion_full":  # traffic.json describes the config-3 launches only
+                traffic.setdefault(key, []).append(b)
             txt.append(f"    {'dram bytes read + write':60s} {b:18.0f} byte")
             dur = float(d["gpu__time_duration.sum"].replace(",", ""))
             dur_s = dur * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(
