@@ -20,4 +20,9 @@ python tools/prof_fusion.py --layout mlp10m --dtype f32 --runs 3 > $OUT/prof_c1_
 ncu --set full --clock-control none --import-source on -k "regex:k_merge|k_sumsq" -s 2 -c 2 -o $OUT/config1_full python tools/prof_fusion.py --layout mlp10m --dtype f32 --runs 3 > $OUT/ncu_config1.log 2>&1
 python tools/step_gap.py > $OUT/step_gap.log 2>&1
 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1
+# .ncu-rep files are large (gpurun copies back at most 64 MiB): keep their raw metric pages as CSV
+for rep in fusion_full grpo_full config1_full; do
+  [ -f $OUT/$rep.ncu-rep ] && ncu -i $OUT/$rep.ncu-rep --page raw --csv > $OUT/$rep.raw.csv 2>/dev/null && rm -f $OUT/$rep.ncu-rep
+done
 ls -la $OUT
+du -sh gpurun_out

@@ -66,9 +66,12 @@ traffic = {}
 for rep, out in (("fusion_full", "ncu_fusion_summary"), ("grpo_full", "ncu_grpo_summary"),
                  ("config1_full", "ncu_config1_summary")):
     f = src / f"{rep}.ncu-rep"
-    if not f.exists():
+    if (src / f"{rep}.raw.csv").exists():  # exported on the GPU box (profile_round.sh)
+        raw = (src / f"{rep}.raw.csv").read_text()
+    elif f.exists():
+        raw = subprocess.run(["ncu", "-i", str(f), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    else:
         continue
-    raw = subprocess.run(["ncu", "-i", str(f), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     h, units = rr[0], rr[1]
     txt = [f"# ncu --set full --clock-control none ({rep}.ncu-rep): key metrics per captured launch", ""]
