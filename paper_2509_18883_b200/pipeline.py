@@ -245,7 +245,8 @@ def pack_batch(groups: Sequence[Group], t_max: int, *, rep_cfg=None, adv_cfg=Non
             if len(s.infer_logps) < n:
                 raise ValueError(f"sample of prompt {s.prompt_id} has fewer infer_logps than tokens")
             toks.extend(int(t) for t in s.tokens)
-            lt.extend(float(x) for x in s.train_logps[:n]) if live else lt.extend([0.0] * n)
+            # masked samples' rows are never read by the kernels; their train log-probs may be absent
+            lt.extend([float(x) for x in s.train_logps[:n]] if live else [0.0] * n)
             li.extend(float(x) for x in s.infer_logps[:n])
             cu.append(len(toks))
             adv.append(float(a))
