@@ -457,3 +457,27 @@ def test_f32_specialised_merge_vs_oracle(cuda, n, cfgkw):
         st = rep.stats(name)
         assert list(st.erased_counts) == rstats[name]["erased"] == list(rep_x.stats(name).erased_counts), name
         assert list(st.dropout_kept_fraction) == rstats[name]["kept"], name
+
+
+def test_empty_tables_match_reference(cuda):
+    """Zero-size tables behave like the reference (checked against rolloutlab here): the task vector's
+    norm is 0, mean normalisation raises its ValueError, and without normalisation the kept fraction
+    0/0 raises ZeroDivisionError; in a state dict, empty tensors pass through beside fused ones."""
+    from paper_2509_18883_b200 import fusion as F
+    b = _pt(np.zeros(0), torch.float64, cuda)
+    t = F.task_vector(_pt(np.zeros(0), torch.float64, cuda), b)
+    assert t.norm == 0.0
+    with pytest.raises(ValueError, match="cannot take mean norm of all-zero task vectors"):
+        F.fuse(b, [t, t], F.FusionConfig())
+    for cfg in (F.FusionConfig(target_norm=None), F.FusionConfig(dropout_p=0.5, target_norm=1.0)):
+        with pytest.raises(ZeroDivisionError):
+            F.fuse(b, [t, t], cfg)
+    g = np.random.default_rng(4)
+    base = {"e0": np.zeros(0), "w": bf16_round(g.normal(0, 0.02, 4096)), "e1": np.zeros((3, 0))}
+    experts = [{k: (bf16_round(v + g.normal(0, 1e-3, v.shape)) if v.size else v) for k, v in base.items()}
+               for _ in range(3)]
+    to = lambda d: {k: torch.from_numpy(np.asarray(v)).to(cuda, torch.bfloat16) for k, v in d.items()}
+    outs, rep = F.fuse_state_dict(to(base), [to(e) for e in experts], F.FusionConfig(dropout_p=0.5, seed=1))
+    assert outs["e0"].shape == (0,) and outs["e1"].shape == (3, 0)
+    ref, _ = OF.fuse(base["w"], [e["w"] for e in experts], dropout_p=0.5, seed=1)
+    assert (outs["w"].view(torch.int16).cpu().numpy().view(np.uint16) != rne_bf16_bits(ref)).sum() == 0
