@@ -368,3 +368,24 @@ def test_objective_mask_branches_vs_reference(cuda, cname):
     assert J == pytest.approx(float(z[f"{cname}/value"][0]), rel=1e-12, abs=1e-16)
     grad = O.objective_gradient(batch, params, clip).cpu().numpy()
     np.testing.assert_allclose(grad, z[f"{cname}/grad"], rtol=1e-10, atol=1e-16)
+
+
+@pytest.mark.parametrize("V", [1000, 250000])
+def test_forward_backward_fallback_shapes(cuda, V):
+    """Vocabularies the cluster kernel does not take (V % 16 != 0, V > 204,800) go through K4 + K5 with the
+    same results: J and every gradient entry against the f64 oracle."""
+    from paper_2509_18883_b200 import objective as O
+    G, S, Rps, T_max = 4, 4, 5, 8
+    logits, toks, lt, li, adv, use, cu = _synthetic_rows(Rps, S, V, G, seed=6, tau=1.0, masked=(1,))
+    b = O.GRPOBatch.pack(toks, lt, li, cu, adv, use, G, T_max, device=cuda)
+    lg = torch.from_numpy(logits).to(cuda, torch.bfloat16)
+    fwd, grad = O.grpo_forward_backward(lg, b)
+    clip = dict(eps_neg_low=0.2, eps_pos_high=0.2, eps_neg_high=3.0, tis_cap=2.0, guard_positive=True)
+    sor = np.repeat(np.arange(S), Rps)
+    norm = 1.0 / ((S // G) * G * T_max)
+    logp, term, coef = OO.token_terms(logits, None, toks, lt, li, sor, adv, use, [1.0] * S, clip, norm=norm)
+    J = OO.objective(term, list(cu[::G]), G, T_max)
+    assert float(fwd.objective) == pytest.approx(J, rel=1e-3)
+    cg = fwd.coef.cpu().numpy()
+    rtol = 5e-6 if grad.dtype == torch.float32 else 2.0 ** -8 + 5e-6
+    assert_grad_rows(grad.double().cpu().numpy(), logits, toks, cg, [1.0] * len(toks), rtol)
