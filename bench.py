@@ -101,6 +101,11 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------- distributed
+def _backend_name(group) -> str:
+    import torch.distributed as dist
+    return str(dist.get_backend(group)).upper()
+
+
 def dist_setup(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -890,7 +895,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-hash normal, SURVEY 8(d))",
         "config": {"workload": workload, "params": total, "tensors": fz["n_tensors"], "experts": N_EXPERTS,
-                   "parallelism": f"param-range shards x{world} (embedding-sized tensors striped), NCCL all_reduce of norm partials",
+                   "parallelism": f"param-range shards x{world} (embedding-sized tensors striped), "
+                                  + (f"{_backend_name(group)} all_reduce of the split tensors' norm partials"
+                                     if group is not None else "no collective at one rank"),
                    "l2": fz["l2"], "launch": fz["launch"],
                    "dropout_mode": {1: "inline", 2: "bitmap"}.get(fz["dropout_mode"], "none")},
         "hbm_gbs_step": step_gbs, "hbm_frac_step": step_gbs / peak,
