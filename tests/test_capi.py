@@ -79,3 +79,16 @@ def test_missing_library_fails_loudly(tmp_path):
     env = dict(os.environ, RLK_LIB_PATH=str(tmp_path / "absent.so"), RLK_AUTOBUILD="0")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, env=env, timeout=300)
     assert "RAISED" in out.stdout and "no CPU fallback" in out.stdout, out.stdout + out.stderr
+
+
+def test_integration_ctypes_stub_binds():
+    """The ctypes stub INTEGRATION.md shows a maintainer binds every symbol it names (no GPU calls)."""
+    import re
+    from paper_2509_18883_b200 import _lib
+    if not _lib.LIB_PATH.exists():
+        from paper_2509_18883_b200._build import build
+        build()
+    text = (ROOT / "INTEGRATION.md").read_text()
+    stub = next(b for b in re.findall(r"```python\n(.*?)```", text, re.S) if "C.CDLL" in b)
+    stub = stub.replace('"paper_2509_18883_b200/_rlk.so"', repr(str(_lib.LIB_PATH)))
+    exec(compile(stub, "INTEGRATION.md", "exec"), {})
